@@ -1,0 +1,220 @@
+"""ctypes marshalling for oracle/sgm_oracle.c (test infrastructure only).
+
+No arithmetic of the method lives here: every function allocates numpy outputs,
+passes pointers to the C oracle and returns the arrays.  See sgm_oracle.c for
+the citations of each step.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sgm_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB
+
+
+def build(force: bool = False) -> str:
+    """Compile sgm_oracle.c with gcc -O2 -ffp-contract=off (no SIMD intrinsics)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-std=c11", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _get():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            P = ctypes.c_void_p
+            I = ctypes.c_int
+            L = ctypes.c_int64
+            Dd = ctypes.c_double
+            lib.orc_census.argtypes = [P, I, I, L, I, I, P]
+            lib.orc_cost.argtypes = [P, P, I, I, I, I, I, P]
+            lib.orc_path.argtypes = [P, I, I, I, I, I, I, I, P]
+            lib.orc_aggregate.argtypes = [P, I, I, I, I, I, P]
+            lib.orc_wta.argtypes = [P, I, I, I, P, P]
+            lib.orc_lr_check.argtypes = [P, P, P, I, I, I, I, P, P, P]
+            lib.orc_sgm_view.argtypes = [P, P, I, I, I, I, I, I, I, P, P, P, P]
+            lib.orc_disparity.argtypes = [P, P, I, I, L, I, I, I, I, I, I, I,
+                                          P, P, P, P, P, P, P]
+            lib.orc_combine.argtypes = [P, P, P, P, P, P, I, I, I, P, P]
+            lib.orc_reproject.argtypes = [P, P, I, I, Dd, Dd, Dd, Dd, P, P, P, P]
+            for fn in ("orc_census", "orc_cost", "orc_path", "orc_aggregate", "orc_wta",
+                       "orc_lr_check", "orc_sgm_view", "orc_disparity", "orc_combine",
+                       "orc_reproject"):
+                getattr(lib, fn).restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _p(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def _chk(rc, what):
+    if rc != 0:
+        raise ValueError(f"oracle {what} failed with code {rc}")
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def census(img, cw, ch):
+    img = _c(img, np.uint8)
+    H, W = img.shape
+    out = np.empty((H, W), np.uint64)
+    _chk(_get().orc_census(_p(img), W, H, W, cw, ch, _p(out)), "census")
+    return out
+
+
+def cost(cen_ref, cen_match, D, s, cmax):
+    cen_ref = _c(cen_ref, np.uint64)
+    cen_match = _c(cen_match, np.uint64)
+    H, W = cen_ref.shape
+    out = np.empty((H, W, D), np.uint8)
+    _chk(_get().orc_cost(_p(cen_ref), _p(cen_match), W, H, D, s, cmax, _p(out)), "cost")
+    return out
+
+
+def path(cost_vol, P1, P2, rx, ry):
+    cost_vol = _c(cost_vol, np.uint8)
+    H, W, D = cost_vol.shape
+    out = np.empty((H, W, D), np.int32)
+    _chk(_get().orc_path(_p(cost_vol), W, H, D, P1, P2, rx, ry, _p(out)), "path")
+    return out
+
+
+def aggregate(cost_vol, P1, P2):
+    cost_vol = _c(cost_vol, np.uint8)
+    H, W, D = cost_vol.shape
+    out = np.empty((H, W, D), np.uint32)
+    _chk(_get().orc_aggregate(_p(cost_vol), W, H, D, P1, P2, _p(out)), "aggregate")
+    return out
+
+
+def wta(S):
+    S = _c(S, np.uint32)
+    H, W, D = S.shape
+    di = np.empty((H, W), np.int16)
+    ds = np.empty((H, W), np.float64)
+    _chk(_get().orc_wta(_p(S), W, H, D, _p(di), _p(ds)), "wta")
+    return di, ds
+
+
+def lr_check(dl_int, dl_sub, dr_int, T, invalid=-1):
+    dl_int = _c(dl_int, np.int16)
+    dl_sub = _c(dl_sub, np.float64)
+    dr_int = _c(dr_int, np.int16)
+    H, W = dl_int.shape
+    oi = np.empty((H, W), np.int16)
+    os_ = np.empty((H, W), np.float64)
+    v = np.empty((H, W), np.uint8)
+    _chk(_get().orc_lr_check(_p(dl_int), _p(dl_sub), _p(dr_int), W, H, T, invalid,
+                             _p(oi), _p(os_), _p(v)), "lr_check")
+    return oi, os_, v
+
+
+def sgm_view(cen_ref, cen_match, D, s, cmax, P1, P2, want_cost=False, want_S=False):
+    cen_ref = _c(cen_ref, np.uint64)
+    cen_match = _c(cen_match, np.uint64)
+    H, W = cen_ref.shape
+    di = np.empty((H, W), np.int16)
+    ds = np.empty((H, W), np.float64)
+    C = np.empty((H, W, D), np.uint8) if want_cost else None
+    S = np.empty((H, W, D), np.uint32) if want_S else None
+    _chk(_get().orc_sgm_view(_p(cen_ref), _p(cen_match), W, H, D, s, cmax, P1, P2,
+                             _p(di), _p(ds), _p(C), _p(S)), "sgm_view")
+    return di, ds, C, S
+
+
+def disparity(left, right, D, cw, ch, P1, P2, T, invalid=-1):
+    """Full SGM on one rectified pair.  Returns dict with LR-checked and raw maps."""
+    left = _c(left, np.uint8)
+    right = _c(right, np.uint8)
+    H, W = left.shape
+    out = {
+        "d_int": np.empty((H, W), np.int16), "d_sub": np.empty((H, W), np.float64),
+        "valid": np.empty((H, W), np.uint8),
+        "dl_int": np.empty((H, W), np.int16), "dl_sub": np.empty((H, W), np.float64),
+        "dr_int": np.empty((H, W), np.int16), "dr_sub": np.empty((H, W), np.float64),
+    }
+    _chk(_get().orc_disparity(_p(left), _p(right), W, H, W, D, cw, ch, P1, P2, T, invalid,
+                              _p(out["d_int"]), _p(out["d_sub"]), _p(out["valid"]),
+                              _p(out["dl_int"]), _p(out["dl_sub"]),
+                              _p(out["dr_int"]), _p(out["dr_sub"])), "disparity")
+    return out
+
+
+def combine(d0, v0, d1, v1, flow, flow_valid=None, rule=0):
+    d0 = _c(d0, np.float64)
+    d1 = _c(d1, np.float64)
+    v0 = _c(v0, np.uint8)
+    v1 = _c(v1, np.uint8)
+    flow = _c(flow, np.float32)
+    fv = None if flow_valid is None else _c(flow_valid, np.uint8)
+    H, W = d0.shape
+    sf = np.empty((H, W, 4), np.float64)
+    valid = np.empty((H, W), np.uint8)
+    _chk(_get().orc_combine(_p(d0), _p(v0), _p(d1), _p(v1), _p(flow), _p(fv), W, H, rule,
+                            _p(sf), _p(valid)), "combine")
+    return sf, valid
+
+
+def reproject(sf, valid_sf, f, B, cx, cy):
+    sf = _c(sf, np.float64)
+    valid_sf = _c(valid_sf, np.uint8)
+    H, W, _ = sf.shape
+    p0 = np.empty((H, W, 3), np.float64)
+    p1 = np.empty((H, W, 3), np.float64)
+    dp = np.empty((H, W, 3), np.float64)
+    v3 = np.empty((H, W), np.uint8)
+    _chk(_get().orc_reproject(_p(sf), _p(valid_sf), W, H, f, B, cx, cy,
+                              _p(p0), _p(p1), _p(dp), _p(v3)), "reproject")
+    return p0, p1, dp, v3
+
+
+def run_quad(quad, prm, rule=0, threads=True):
+    """The whole hot path on one frame quadruple: SGM at t and t+1,
+    combination Eq. (4)/(5), 3D.  ``quad`` holds il0, ir0, il1, ir1, flow;
+    ``prm`` holds D, cw, ch, P1, P2, T, f, B (and optional cx, cy)."""
+    args = (prm["D"], prm["cw"], prm["ch"], prm["P1"], prm["P2"], prm["T"])
+    res = {}
+
+    def run(key, l, r):
+        res[key] = disparity(l, r, *args)
+
+    if threads:
+        th = [threading.Thread(target=run, args=("t0", quad["il0"], quad["ir0"])),
+              threading.Thread(target=run, args=("t1", quad["il1"], quad["ir1"]))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    else:
+        run("t0", quad["il0"], quad["ir0"])
+        run("t1", quad["il1"], quad["ir1"])
+    H, W = quad["il0"].shape
+    cx = prm.get("cx", (W - 1) / 2.0)
+    cy = prm.get("cy", (H - 1) / 2.0)
+    sf, vsf = combine(res["t0"]["d_sub"], res["t0"]["valid"], res["t1"]["d_sub"],
+                      res["t1"]["valid"], quad["flow"], None, rule)
+    p0, p1, dp, v3 = reproject(sf, vsf, prm["f"], prm["B"], cx, cy)
+    return {"disp0": res["t0"], "disp1": res["t1"], "sf": sf, "valid_sf": vsf,
+            "p0": p0, "p1": p1, "dp": dp, "valid_3d": v3}
