@@ -1,0 +1,219 @@
+/*
+ * sgmsf.h -- C ABI of the B200 (sm_100a) SGM stereo + basic scene flow library
+ * (libsgmsf.so), implementing the hot path of Schuster et al., "Combining
+ * Stereo Disparity and Optical Flow for Basic Scene Flow" (arXiv 1801.04720).
+ *
+ * Citations: P:n = PAPER.md line n (section / equation given), S:n = SPEC.md
+ * line n, G# = reading
+ *
+ * General conventions
+ *  - Every pointer argument is DEVICE memory of the handle's device unless the
+ *    function name ends in _host.  The caller owns every input and output
+ *    buffer; the handle owns only its scratch (allocated once in sgm_create).
+ *    Nothing is allocated per call.
+ *  - Layouts are row-major [H][W] (x fastest), with a trailing channel /
+ *    disparity dimension where stated.  Images may carry a row pitch; every
+ *    other buffer is dense.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call only enqueues work on `stream` and returns without a host
+ *    synchronisation (except sgm_create / sgm_destroy).  Asynchronous device
+ *    faults surface at the caller's next synchronisation.
+ *  - Argument errors are detected synchronously, before anything is enqueued,
+ *    and return SGM_ERR_INVALID_ARGUMENT.  Launch failures return
+ *    SGM_ERR_CUDA.  No C++ exception crosses this ABI.
+ *  - A handle is bound to one device and is not re-entrant: use one handle per
+ *    concurrent stream.  Identical inputs give bit-identical outputs.
+ */
+#ifndef SGMSF_H
+#define SGMSF_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SGM_API __attribute__((visibility("default")))
+#else
+#define SGM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sgm_status {
+    SGM_OK = 0,
+    SGM_ERR_INVALID_ARGUMENT = 1,
+    SGM_ERR_UNSUPPORTED = 2,
+    SGM_ERR_CUDA = 3,
+    SGM_ERR_OUT_OF_MEMORY = 4
+} sgm_status;
+
+/* Method parameters (BASELINE.json configs). */
+typedef struct sgm_params {
+    int32_t width;          /* W >= 1: the shared image domain Omega */
+    int32_t height;         /* H >= 1 */
+    int32_t num_disp;       /* D disparity levels, d in [0, D-1] (G6); 1 <= D <= 256 */
+    int32_t census_w;       /* census window width, odd (G2) */
+    int32_t census_h;       /* census window height, odd; census_w*census_h-1 <= 64 */
+    int32_t p1;             /* small-jump penalty P1, 0 <= P1 <= P2 (G8) */
+    int32_t p2;             /* large-jump penalty P2; C_max + P2 <= 255 where
+                               C_max = census_w*census_h-1 (G5, G9) */
+    int32_t lr_threshold;   /* T >= 0, integer pixels (G13) */
+    int32_t invalid_disp;   /* value written for invalid disparities (G14: -1) */
+    int32_t bilinear_rule;  /* 0: taps with nonzero weight must be valid (G18);
+                               1: all four taps valid (SPEC D-2) */
+    int32_t max_batch;      /* >= 1: most frame quads one sgm_scene_flow call takes
+                               (sizes the scratch) */
+} sgm_params;
+
+/* Pinhole camera of the rectified rig ("camera intrinsics and extrinsics";
+ * G19/G20).  X right, Y down, Z forward, metres. */
+typedef struct sgm_camera {
+    float f_px;             /* focal length in pixels, > 0 */
+    float baseline_m;       /* stereo baseline in metres, > 0 */
+    float cx, cy;           /* principal point in pixels */
+} sgm_camera;
+
+typedef struct sgm_handle sgm_handle;
+
+/* Result buffers of sgm_scene_flow (Eq. (3)/(4), P:96/P:118 3D).
+ * Any pointer except sf and valid_sf may be NULL to skip that output. */
+typedef struct sgm_sceneflow_out {
+    float   *sf;            /* [n][H][W][4] = (u, v, d0, d1) (Eq. (3)); 0 where invalid */
+    uint8_t *valid_sf;      /* [n][H][W] 1 = S(x) defined (Eq. (4)) */
+    float   *p0;            /* [n][H][W][4] = (X, Y, Z, 0) of x at t (NULL: skip 3D) */
+    float   *dp;            /* [n][H][W][4] = (dX, dY, dZ, 0) motion (NULL: skip 3D) */
+    uint8_t *valid_3d;      /* [n][H][W] 1 = S valid and d0 > 0 and d1 > 0 (G21) */
+    int16_t *disp_int;      /* [n][2][H][W] LR-checked integer D0 (t), D1 (t+1) */
+    float   *disp_sub;      /* [n][2][H][W] LR-checked sub-pixel D0, D1 (-1 invalid) */
+    uint8_t *disp_valid;    /* [n][2][H][W] LR masks of D0, D1 */
+} sgm_sceneflow_out;
+
+/* Create a handle on `device` (cudaSetDevice is called): validates `p`
+ * (SGM_ERR_INVALID_ARGUMENT on: W or H < 1, D outside 1..256, even census
+ * side, census_w*census_h-1 > 64, P1 < 0, P2 < P1, C_max+P2 > 255, T < 0,
+ * bilinear_rule not 0/1, max_batch < 1) and allocates all scratch for
+ * max_batch quads (SGM_ERR_OUT_OF_MEMORY if that fails).  Synchronous.
+ * `*out` is set only on SGM_OK. */
+SGM_API sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out);
+
+/* Free the handle and its scratch after synchronising the device.  NULL-safe. */
+SGM_API void sgm_destroy(sgm_handle *h);
+
+/* Static description of a status code (never NULL). */
+SGM_API const char *sgm_status_string(sgm_status s);
+
+/* Census transform of one uint8 image (G2-G4): out[y][x] bit k =
+ * [neighbour k < centre] over the census_w x census_h window scanned row-major
+ * (dy outer, dx inner), centre skipped, coordinates clamped to the image.
+ * img: [H] rows of `pitch_bytes` (pitch >= W, pitch % 16 == 0, img 16-byte
+ * aligned: the tile is staged by TMA).  census: [H][W] uint64, LSB = bit 0. */
+SGM_API sgm_status sgm_census(sgm_handle *h, const uint8_t *img, int64_t pitch_bytes,
+                      uint64_t *census, void *stream);
+
+/* Matching cost volume of one view (G5, G12), debug / parity path:
+ * view 0 (left reference): C(x,y,d) = popcount(cen_left(x,y) ^ cen_right(x-d,y));
+ * view 1 (right reference): C(x,y,d) = popcount(cen_right(x,y) ^ cen_left(x+d,y));
+ * a match outside the image costs C_max = census_w*census_h-1.
+ * cost: [H][W][D] uint8. */
+SGM_API sgm_status sgm_cost(sgm_handle *h, const uint64_t *cen_left, const uint64_t *cen_right,
+                    int32_t view, uint8_t *cost, void *stream);
+
+/* Aggregated cost S = sum over the 8 paths (recursion S:129,
+ * G7) of one view, computed by the fused cost+aggregation sweeps and
+ * materialised for parity: agg [H][W][D] uint16 (S <= 8*(C_max+P2), G9).
+ * view as in sgm_cost.  Uses the handle's view-0 scratch. */
+SGM_API sgm_status sgm_aggregate(sgm_handle *h, const uint64_t *cen_left, const uint64_t *cen_right,
+                         int32_t view, uint16_t *agg, void *stream);
+
+/* Winner-take-all + parabola sub-pixel (G10/G11) on a materialised
+ * agg [H][W][D] uint16: d_int = smallest argmin, d_sub = d_int + (a-c)/(2(a+c-2b))
+ * for 0 < d_int < D-1 (float32, IEEE division), else d_int.  Every pixel gets a
+ * value.  d_int [H][W] int16, d_sub [H][W] float32. */
+SGM_API sgm_status sgm_wta(sgm_handle *h, const uint16_t *agg, int16_t *d_int, float *d_sub,
+                   void *stream);
+
+/* Left-right consistency check (integer reading G13):
+ * valid(x,y) iff x - dl(x,y) >= 0 and |dl(x,y) - dr(x - dl(x,y), y)| <= T.
+ * out_int / out_sub = dl_int / dl_sub where valid, else invalid_disp; valid
+ * [H][W] uint8.  dl_int, dr_int [H][W] int16 raw WTA maps of the left- and
+ * right-reference views; dl_sub [H][W] float32. */
+SGM_API sgm_status sgm_lr_check(sgm_handle *h, const int16_t *dl_int, const float *dl_sub,
+                        const int16_t *dr_int, int16_t *out_int, float *out_sub,
+                        uint8_t *valid, void *stream);
+
+/* Whole SGM on one rectified pair: census of both
+ * images, fused cost+8-path aggregation of the left- and right-reference views,
+ * WTA + sub-pixel, LR check.  Equals the stage-wise composition
+ * sgm_census -> sgm_aggregate -> sgm_wta -> sgm_lr_check bit for bit.
+ * left/right as in sgm_census (same pitch); outputs as in sgm_lr_check. */
+SGM_API sgm_status sgm_disparity(sgm_handle *h, const uint8_t *left, const uint8_t *right,
+                         int64_t pitch_bytes, int16_t *out_int, float *out_sub,
+                         uint8_t *valid, void *stream);
+
+/* Combination Eq. (4) with the bilinear warp of Eq. (5) and the 3D
+ * interpretation (G15-G23):
+ *   x' = x + F(x) in float32; defined iff F valid, d0 valid, 0 <= x' <= W-1,
+ *   0 <= y' <= H-1 and D1 valid on the bilinear footprint (bilinear_rule);
+ *   sf = (u, v, d0(x), D1(x')) else 0;  Z = f B / d, X = (x-cx) Z / f,
+ *   Y = (y-cy) Z / f; p0 from (x, d0), end point from (x', d1), dp = P1 - P0;
+ *   valid_3d = valid_sf and d0 > 0 and d1 > 0.
+ * d0, d1 [H][W] float32 (LR-checked sub-pixel maps at t, t+1); v0, v1 [H][W]
+ * uint8; flow [H][W][2] float32 (u, v); flow_valid nullable (all valid, G23);
+ * sf [H][W][4]; p0, dp [H][W][4] nullable (skip 3D; then valid_3d may be NULL).
+ */
+SGM_API sgm_status sgm_combine_sceneflow(sgm_handle *h, const float *d0, const uint8_t *v0,
+                                 const float *d1, const uint8_t *v1, const float *flow,
+                                 const uint8_t *flow_valid, const sgm_camera *cam,
+                                 float *sf, float *p0, float *dp, uint8_t *valid_sf,
+                                 uint8_t *valid_3d, void *stream);
+
+/* The whole hot path for n independent frame quadruples (Fig. 2):
+ * SGM at t and t+1 (4 census images, 4 views, 2 LR checks) and the
+ * combination + 3D, as 5 kernel launches for the whole batch.
+ * images: [n][4][H] rows of pitch_bytes, order I_l^t, I_r^t, I_l^{t+1},
+ * I_r^{t+1} (pitch % 16 == 0, 16-byte aligned); flow: [n][H][W][2];
+ * flow_valid: [n][H][W] or NULL; 1 <= n <= max_batch. */
+SGM_API sgm_status sgm_scene_flow(sgm_handle *h, int32_t n, const uint8_t *images, int64_t pitch_bytes,
+                          const float *flow, const uint8_t *flow_valid,
+                          const sgm_camera *cam, const sgm_sceneflow_out *out, void *stream);
+
+/* Same as sgm_scene_flow but every buffer (inputs and the non-NULL outputs of
+ * *out) is HOST memory, densely packed ([n][4][H][W] images): the call
+ * enqueues host->device copies into the handle's staging buffers, the
+ * pipeline, and device->host copies of the requested outputs on `stream`.
+ * Use page-locked host memory for asynchronous copies; the results are
+ * available after the caller synchronises `stream`. */
+SGM_API sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images,
+                               const float *flow, const uint8_t *flow_valid,
+                               const sgm_camera *cam, const sgm_sceneflow_out *out,
+                               void *stream);
+
+/* ---- instrumentation ----------------------------------------------------- */
+enum { SGM_NUM_STAGES = 5 };   /* census, sweep_fwd, sweep_bwd_wta, lr_check, combine */
+
+/* Enable (1) / disable (0) CUDA-event timing of every kernel that
+ * sgm_scene_flow / sgm_scene_flow_host enqueue (events are recorded on the
+ * launch stream, also inside CUDA-graph capture). */
+SGM_API sgm_status sgm_set_timing(sgm_handle *h, int32_t enable);
+
+/* After the caller synchronised the stream: per-stage durations (ms) of the
+ * last timed sgm_scene_flow call into ms[SGM_NUM_STAGES].  Returns the number
+ * of stages written (0 if timing was off or nothing ran). */
+SGM_API int32_t sgm_read_timing(sgm_handle *h, float *ms);
+
+/* Static stage name for index 0..SGM_NUM_STAGES-1 ("?" otherwise). */
+SGM_API const char *sgm_stage_name(int32_t stage);
+
+/* Number of kernels this handle has launched so far (all entry points). */
+SGM_API int64_t sgm_launch_count(sgm_handle *h);
+
+/* Internal geometry, for tests and roofline accounting: padded disparity
+ * count Dp (multiple of 64), cells per lane, warps per CTA of the sweeps,
+ * rows per band. Any pointer may be NULL. */
+SGM_API sgm_status sgm_get_geometry(sgm_handle *h, int32_t *dp, int32_t *cells_per_lane,
+                            int32_t *sweep_warps, int32_t *band_rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGMSF_H */

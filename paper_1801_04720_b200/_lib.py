@@ -1,0 +1,129 @@
+"""ctypes binding of libsgmsf.so (include/sgmsf.h): argument marshalling only.
+
+Every step of the method runs in the library's CUDA kernels; this module turns
+Python ints / pointers into the C types of the ABI and raises on non-OK
+status.  It never falls back to any other implementation: if the library is
+missing or fails to load, ``load()`` raises ``SgmLibraryError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import build as _build
+
+LIB_PATH = _build.LIB
+
+SGM_OK = 0
+STATUS = {0: "SGM_OK", 1: "SGM_ERR_INVALID_ARGUMENT", 2: "SGM_ERR_UNSUPPORTED", 3: "SGM_ERR_CUDA",
+          4: "SGM_ERR_OUT_OF_MEMORY"}
+NUM_STAGES = 5
+
+# Every symbol include/sgmsf.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "sgm_create", "sgm_destroy", "sgm_status_string", "sgm_census", "sgm_cost", "sgm_aggregate",
+    "sgm_wta", "sgm_lr_check", "sgm_disparity", "sgm_combine_sceneflow", "sgm_scene_flow",
+    "sgm_scene_flow_host", "sgm_set_timing", "sgm_read_timing", "sgm_stage_name",
+    "sgm_launch_count", "sgm_get_geometry",
+)
+
+
+class SgmLibraryError(RuntimeError):
+    pass
+
+
+class SgmError(RuntimeError):
+    def __init__(self, fn, code, lib=None):
+        msg = STATUS.get(code, str(code))
+        if lib is not None:
+            try:
+                msg += ": " + lib.sgm_status_string(code).decode()
+            except Exception:  # pragma: no cover
+                pass
+        super().__init__(f"{fn} failed: {msg}")
+        self.code = code
+
+
+class SgmParams(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("num_disp", ctypes.c_int32), ("census_w", ctypes.c_int32),
+                ("census_h", ctypes.c_int32), ("p1", ctypes.c_int32), ("p2", ctypes.c_int32),
+                ("lr_threshold", ctypes.c_int32), ("invalid_disp", ctypes.c_int32),
+                ("bilinear_rule", ctypes.c_int32), ("max_batch", ctypes.c_int32)]
+
+
+class SgmCamera(ctypes.Structure):
+    _fields_ = [("f_px", ctypes.c_float), ("baseline_m", ctypes.c_float),
+                ("cx", ctypes.c_float), ("cy", ctypes.c_float)]
+
+
+class SgmSceneflowOut(ctypes.Structure):
+    _fields_ = [("sf", ctypes.c_void_p), ("valid_sf", ctypes.c_void_p),
+                ("p0", ctypes.c_void_p), ("dp", ctypes.c_void_p),
+                ("valid_3d", ctypes.c_void_p), ("disp_int", ctypes.c_void_p),
+                ("disp_sub", ctypes.c_void_p), ("disp_valid", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load libsgmsf.so (building it first if the sources are newer and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or LIB_PATH
+    if not os.path.exists(path) or not _build.up_to_date():
+        if os.path.exists(_build.NVCC):
+            _build.build()
+    if not os.path.exists(path):
+        raise SgmLibraryError(f"{path} is missing: run `python -m paper_1801_04720_b200.build`")
+    try:
+        lib = ctypes.CDLL(path)
+    except OSError as e:
+        raise SgmLibraryError(f"cannot load {path}: {e}") from e
+    P = ctypes.c_void_p
+    I32 = ctypes.c_int32
+    I64 = ctypes.c_int64
+    st = ctypes.c_int
+    sig = {
+        "sgm_create": (st, [ctypes.POINTER(SgmParams), I32, ctypes.POINTER(P)]),
+        "sgm_destroy": (None, [P]),
+        "sgm_status_string": (ctypes.c_char_p, [st]),
+        "sgm_census": (st, [P, P, I64, P, P]),
+        "sgm_cost": (st, [P, P, P, I32, P, P]),
+        "sgm_aggregate": (st, [P, P, P, I32, P, P]),
+        "sgm_wta": (st, [P, P, P, P, P]),
+        "sgm_lr_check": (st, [P, P, P, P, P, P, P, P]),
+        "sgm_disparity": (st, [P, P, P, I64, P, P, P, P]),
+        "sgm_combine_sceneflow": (st, [P, P, P, P, P, P, P, ctypes.POINTER(SgmCamera), P, P, P,
+                                       P, P, P]),
+        "sgm_scene_flow": (st, [P, I32, P, I64, P, P, ctypes.POINTER(SgmCamera),
+                                ctypes.POINTER(SgmSceneflowOut), P]),
+        "sgm_scene_flow_host": (st, [P, I32, P, P, P, ctypes.POINTER(SgmCamera),
+                                     ctypes.POINTER(SgmSceneflowOut), P]),
+        "sgm_set_timing": (st, [P, I32]),
+        "sgm_read_timing": (I32, [P, ctypes.POINTER(ctypes.c_float)]),
+        "sgm_stage_name": (ctypes.c_char_p, [I32]),
+        "sgm_launch_count": (I64, [P]),
+        "sgm_get_geometry": (st, [P, ctypes.POINTER(I32), ctypes.POINTER(I32),
+                                  ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(fn_name: str, code: int):
+    if code != SGM_OK:
+        raise SgmError(fn_name, code, _lib)
+
+
+def call(name: str, *args):
+    """Call an sgm_* function that returns sgm_status; raise on failure."""
+    lib = load()
+    code = getattr(lib, name)(*args)
+    check(name, code)

@@ -1,0 +1,455 @@
+// api.cu -- the C ABI of libsgmsf.so (include/sgmsf.h): handle, validation, scratch,
+// launch orchestration on the caller's stream, status codes, instrumentation.
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/sgmsf.h"
+#include "sgm_internal.cuh"
+
+namespace sgm {
+cudaError_t launch_census_stack(const uint8_t *base, long long img_stride, int nimg, long long pitch,
+                                int W, int H, int cw, int ch, uint64_t *out, long long out_stride,
+                                cudaStream_t st);
+int sweep_warps_for(int cpl);
+}  // namespace sgm
+
+struct sgm_handle {
+    sgm_params prm;
+    int device = 0;
+    int cpl = 0, dp = 0, nw = 0, nbands = 0;
+    bool c64 = false;
+    int cmax = 0;
+    long long npx = 0;
+    int max_views = 0;
+    // scratch (device)
+    uint64_t *census = nullptr;     // [4*max_batch][H][W]
+    uint16_t *sfwd = nullptr;       // [4*max_batch][H][W][Dp]
+    int16_t *dint = nullptr;        // [4*max_batch][H][W]
+    float *dsub = nullptr;          // [4*max_batch][H][W]
+    int16_t *lr_int = nullptr;      // [2*max_batch][H][W]
+    float *lr_sub = nullptr;
+    uint8_t *lr_valid = nullptr;
+    uint16_t *gbuf = nullptr;       // [4*max_batch][nbands][W][3][Dp]
+    int *sync = nullptr;            // [1 + 4*max_batch*nbands]
+    // staging for the _host entry point (device)
+    uint8_t *img_stage = nullptr;   // [max_batch][4][H][pitch]
+    long long stage_pitch = 0;
+    float *flow_stage = nullptr;    // [max_batch][H][W][2]
+    uint8_t *fvalid_stage = nullptr;
+    float *sf_stage = nullptr, *p0_stage = nullptr, *dp_stage = nullptr;
+    uint8_t *vsf_stage = nullptr, *v3_stage = nullptr;
+    // instrumentation
+    bool timing = false;
+    bool timed = false;
+    cudaEvent_t ev[SGM_NUM_STAGES + 1] = {};
+    long long launches = 0;
+};
+
+namespace {
+
+sgm_status from_cuda(cudaError_t e) {
+    if (e == cudaSuccess) return SGM_OK;
+    if (e == cudaErrorMemoryAllocation) return SGM_ERR_OUT_OF_MEMORY;
+    if (e == cudaErrorInvalidValue) return SGM_ERR_INVALID_ARGUMENT;
+    return SGM_ERR_CUDA;
+}
+
+template <class T>
+cudaError_t dalloc(T **p, size_t count) {
+    return cudaMalloc(reinterpret_cast<void **>(p), count * sizeof(T) + 256);
+}
+
+void free_all(sgm_handle *h) {
+    void *ptrs[] = {h->census, h->sfwd, h->dint, h->dsub, h->lr_int, h->lr_sub, h->lr_valid,
+                    h->gbuf, h->sync, h->img_stage, h->flow_stage, h->fvalid_stage,
+                    h->sf_stage, h->p0_stage, h->dp_stage, h->vsf_stage, h->v3_stage};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    for (auto &e : h->ev)
+        if (e) cudaEventDestroy(e);
+}
+
+sgm::SweepParams sweep_params(const sgm_handle *h, int nviews) {
+    sgm::SweepParams p{};
+    p.W = h->prm.width; p.H = h->prm.height; p.D = h->prm.num_disp; p.Dp = h->dp;
+    p.P1 = h->prm.p1; p.P2 = h->prm.p2; p.cmax = h->cmax;
+    p.nviews = nviews; p.nbands = h->nbands;
+    p.cen = h->census; p.cen_img_stride = h->npx;
+    p.explicit_mode = 0;
+    p.sfwd = h->sfwd; p.sfwd_view_stride = h->npx * h->dp;
+    p.dint = h->dint; p.dsub = h->dsub; p.disp_view_stride = h->npx;
+    p.sout = nullptr;
+    p.gbuf = h->gbuf; p.progress = h->sync + 1; p.ticket = h->sync;
+    return p;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char *sgm_status_string(sgm_status s) {
+    switch (s) {
+        case SGM_OK: return "ok";
+        case SGM_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case SGM_ERR_UNSUPPORTED: return "unsupported";
+        case SGM_ERR_CUDA: return "CUDA error";
+        case SGM_ERR_OUT_OF_MEMORY: return "out of device memory";
+    }
+    return "unknown status";
+}
+
+const char *sgm_stage_name(int32_t stage) {
+    static const char *names[SGM_NUM_STAGES] = {"census", "sweep_fwd", "sweep_bwd_wta", "lr_check",
+                                                "combine"};
+    return (stage >= 0 && stage < SGM_NUM_STAGES) ? names[stage] : "?";
+}
+
+sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
+    if (!p || !out) return SGM_ERR_INVALID_ARGUMENT;
+    const int W = p->width, H = p->height, D = p->num_disp;
+    const int cw = p->census_w, ch = p->census_h;
+    if (W < 1 || H < 1 || D < 1 || D > 256) return SGM_ERR_INVALID_ARGUMENT;
+    if (cw < 1 || ch < 1 || (cw % 2) == 0 || (ch % 2) == 0 || cw * ch - 1 > 64 || cw * ch < 2)
+        return SGM_ERR_INVALID_ARGUMENT;
+    if (cw > 17 || ch > 17) return SGM_ERR_UNSUPPORTED;      // TMA box halo limits
+    if (p->p1 < 0 || p->p2 < p->p1 || (cw * ch - 1) + p->p2 > 255) return SGM_ERR_INVALID_ARGUMENT;
+    if (p->lr_threshold < 0 || (p->bilinear_rule != 0 && p->bilinear_rule != 1) || p->max_batch < 1)
+        return SGM_ERR_INVALID_ARGUMENT;
+    if ((long long)W * H * 4LL * p->max_batch > (1LL << 40)) return SGM_ERR_INVALID_ARGUMENT;
+
+    sgm_handle *h = new (std::nothrow) sgm_handle();
+    if (!h) return SGM_ERR_OUT_OF_MEMORY;
+    h->prm = *p;
+    h->device = device;
+    h->cmax = cw * ch - 1;
+    h->c64 = h->cmax > 32;
+    h->cpl = 2 * ((D + 63) / 64);
+    h->dp = 32 * h->cpl;
+    h->nw = sgm::sweep_warps_for(h->cpl);
+    h->nbands = (H + h->nw - 1) / h->nw;
+    h->npx = (long long)W * H;
+    h->max_views = 4 * p->max_batch;
+
+    cudaError_t e = cudaSetDevice(device);
+    const size_t nv = size_t(h->max_views), npx = size_t(h->npx);
+    h->stage_pitch = ((long long)W + 15) / 16 * 16;
+    if (e == cudaSuccess) e = dalloc(&h->census, nv * npx);
+    if (e == cudaSuccess) e = dalloc(&h->sfwd, nv * npx * size_t(h->dp));
+    if (e == cudaSuccess) e = dalloc(&h->dint, nv * npx);
+    if (e == cudaSuccess) e = dalloc(&h->dsub, nv * npx);
+    if (e == cudaSuccess) e = dalloc(&h->lr_int, nv / 2 * npx);
+    if (e == cudaSuccess) e = dalloc(&h->lr_sub, nv / 2 * npx);
+    if (e == cudaSuccess) e = dalloc(&h->lr_valid, nv / 2 * npx);
+    if (e == cudaSuccess) e = dalloc(&h->gbuf, nv * size_t(h->nbands) * size_t(W) * 3 * size_t(h->dp));
+    if (e == cudaSuccess) e = dalloc(&h->sync, 1 + nv * size_t(h->nbands));
+    if (e == cudaSuccess) e = dalloc(&h->img_stage, nv * size_t(H) * size_t(h->stage_pitch));
+    if (e == cudaSuccess) e = dalloc(&h->flow_stage, size_t(p->max_batch) * npx * 2);
+    if (e == cudaSuccess) e = dalloc(&h->fvalid_stage, size_t(p->max_batch) * npx);
+    if (e == cudaSuccess) e = dalloc(&h->sf_stage, size_t(p->max_batch) * npx * 4);
+    if (e == cudaSuccess) e = dalloc(&h->p0_stage, size_t(p->max_batch) * npx * 4);
+    if (e == cudaSuccess) e = dalloc(&h->dp_stage, size_t(p->max_batch) * npx * 4);
+    if (e == cudaSuccess) e = dalloc(&h->vsf_stage, size_t(p->max_batch) * npx);
+    if (e == cudaSuccess) e = dalloc(&h->v3_stage, size_t(p->max_batch) * npx);
+    for (int i = 0; i <= SGM_NUM_STAGES && e == cudaSuccess; ++i) e = cudaEventCreate(&h->ev[i]);
+    if (e == cudaSuccess) e = cudaMemset(h->sync, 0, sizeof(int) * (1 + nv * size_t(h->nbands)));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        free_all(h);
+        delete h;
+        return from_cuda(e);
+    }
+    *out = h;
+    return SGM_OK;
+}
+
+void sgm_destroy(sgm_handle *h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    free_all(h);
+    delete h;
+}
+
+sgm_status sgm_get_geometry(sgm_handle *h, int32_t *dp, int32_t *cells_per_lane,
+                            int32_t *sweep_warps, int32_t *band_rows) {
+    if (!h) return SGM_ERR_INVALID_ARGUMENT;
+    if (dp) *dp = h->dp;
+    if (cells_per_lane) *cells_per_lane = h->cpl;
+    if (sweep_warps) *sweep_warps = h->nw;
+    if (band_rows) *band_rows = h->nw;
+    return SGM_OK;
+}
+
+int64_t sgm_launch_count(sgm_handle *h) { return h ? h->launches : 0; }
+
+sgm_status sgm_set_timing(sgm_handle *h, int32_t enable) {
+    if (!h) return SGM_ERR_INVALID_ARGUMENT;
+    h->timing = enable != 0;
+    h->timed = false;
+    return SGM_OK;
+}
+
+int32_t sgm_read_timing(sgm_handle *h, float *ms) {
+    if (!h || !ms || !h->timed) return 0;
+    for (int i = 0; i < SGM_NUM_STAGES; ++i) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        ms[i] = t;
+    }
+    return SGM_NUM_STAGES;
+}
+
+sgm_status sgm_census(sgm_handle *h, const uint8_t *img, int64_t pitch_bytes, uint64_t *census,
+                      void *stream) {
+    if (!h || !img || !census || pitch_bytes < h->prm.width || (pitch_bytes % 16) != 0 ||
+        !aligned16(img))
+        return SGM_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = sgm::launch_census_stack(img, (long long)h->prm.height * pitch_bytes, 1,
+                                             pitch_bytes, h->prm.width, h->prm.height,
+                                             h->prm.census_w, h->prm.census_h, census, h->npx, st);
+    if (e == cudaSuccess) ++h->launches;
+    return from_cuda(e);
+}
+
+sgm_status sgm_cost(sgm_handle *h, const uint64_t *cen_left, const uint64_t *cen_right,
+                    int32_t view, uint8_t *cost, void *stream) {
+    if (!h || !cen_left || !cen_right || !cost || (view != 0 && view != 1))
+        return SGM_ERR_INVALID_ARGUMENT;
+    const uint64_t *ref = view == 0 ? cen_left : cen_right;
+    const uint64_t *match = view == 0 ? cen_right : cen_left;
+    cudaError_t e = sgm::launch_cost(ref, match, h->prm.width, h->prm.height, h->prm.num_disp,
+                                     view == 0 ? -1 : 1, h->cmax, cost,
+                                     static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) ++h->launches;
+    return from_cuda(e);
+}
+
+sgm_status sgm_aggregate(sgm_handle *h, const uint64_t *cen_left, const uint64_t *cen_right,
+                         int32_t view, uint16_t *agg, void *stream) {
+    if (!h || !cen_left || !cen_right || !agg || (view != 0 && view != 1))
+        return SGM_ERR_INVALID_ARGUMENT;
+    sgm::SweepParams p = sweep_params(h, 1);
+    p.explicit_mode = 1;
+    p.ref0 = view == 0 ? cen_left : cen_right;
+    p.match0 = view == 0 ? cen_right : cen_left;
+    p.mirror0 = view;
+    p.dint = nullptr;
+    p.dsub = nullptr;
+    p.sout = agg;
+    int n = 0;
+    cudaError_t e = sgm::launch_sweeps(p, h->cpl, h->c64, h->nw, true,
+                                       static_cast<cudaStream_t>(stream), nullptr, nullptr, &n);
+    h->launches += n;
+    return from_cuda(e);
+}
+
+sgm_status sgm_wta(sgm_handle *h, const uint16_t *agg, int16_t *d_int, float *d_sub, void *stream) {
+    if (!h || !agg || !d_int || !d_sub) return SGM_ERR_INVALID_ARGUMENT;
+    cudaError_t e = sgm::launch_wta(agg, h->prm.width, h->prm.height, h->prm.num_disp, d_int, d_sub,
+                                    static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) ++h->launches;
+    return from_cuda(e);
+}
+
+sgm_status sgm_lr_check(sgm_handle *h, const int16_t *dl_int, const float *dl_sub,
+                        const int16_t *dr_int, int16_t *out_int, float *out_sub, uint8_t *valid,
+                        void *stream) {
+    if (!h || !dl_int || !dl_sub || !dr_int || !out_int || !out_sub || !valid)
+        return SGM_ERR_INVALID_ARGUMENT;
+    sgm::LrParams p{};
+    p.W = h->prm.width; p.H = h->prm.height; p.T = h->prm.lr_threshold;
+    p.invalid = h->prm.invalid_disp; p.npairs = 1;
+    p.dl = dl_int; p.dls = dl_sub; p.dr = dr_int;
+    p.in_stride_l = p.in_stride_r = 0;
+    p.out_int = out_int; p.out_sub = out_sub; p.valid = valid; p.out_stride = 0;
+    cudaError_t e = sgm::launch_lr(p, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) ++h->launches;
+    return from_cuda(e);
+}
+
+sgm_status sgm_disparity(sgm_handle *h, const uint8_t *left, const uint8_t *right,
+                         int64_t pitch_bytes, int16_t *out_int, float *out_sub, uint8_t *valid,
+                         void *stream) {
+    if (!h || !left || !right || !out_int || !out_sub || !valid) return SGM_ERR_INVALID_ARGUMENT;
+    if (pitch_bytes < h->prm.width || (pitch_bytes % 16) != 0 || !aligned16(left) ||
+        !aligned16(right))
+        return SGM_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int W = h->prm.width, H = h->prm.height;
+    cudaError_t e = sgm::launch_census_stack(left, (long long)H * pitch_bytes, 1, pitch_bytes, W, H,
+                                             h->prm.census_w, h->prm.census_h, h->census, h->npx, st);
+    if (e == cudaSuccess) {
+        ++h->launches;
+        e = sgm::launch_census_stack(right, (long long)H * pitch_bytes, 1, pitch_bytes, W, H,
+                                     h->prm.census_w, h->prm.census_h, h->census + h->npx, h->npx, st);
+    }
+    if (e == cudaSuccess) {
+        ++h->launches;
+        sgm::SweepParams p = sweep_params(h, 2);
+        int n = 0;
+        e = sgm::launch_sweeps(p, h->cpl, h->c64, h->nw, false, st, nullptr, nullptr, &n);
+        h->launches += n;
+    }
+    if (e == cudaSuccess) {
+        sgm::LrParams p{};
+        p.W = W; p.H = H; p.T = h->prm.lr_threshold; p.invalid = h->prm.invalid_disp; p.npairs = 1;
+        p.dl = h->dint; p.dls = h->dsub; p.dr = h->dint + h->npx;
+        p.out_int = out_int; p.out_sub = out_sub; p.valid = valid;
+        e = sgm::launch_lr(p, st);
+        if (e == cudaSuccess) ++h->launches;
+    }
+    return from_cuda(e);
+}
+
+sgm_status sgm_combine_sceneflow(sgm_handle *h, const float *d0, const uint8_t *v0, const float *d1,
+                                 const uint8_t *v1, const float *flow, const uint8_t *flow_valid,
+                                 const sgm_camera *cam, float *sf, float *p0, float *dp,
+                                 uint8_t *valid_sf, uint8_t *valid_3d, void *stream) {
+    if (!h || !d0 || !v0 || !d1 || !v1 || !flow || !sf || !valid_sf) return SGM_ERR_INVALID_ARGUMENT;
+    const bool want3d = p0 || dp || valid_3d;
+    if (want3d && (!p0 || !dp || !valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
+    if (want3d && !(cam->f_px > 0.f && cam->baseline_m > 0.f)) return SGM_ERR_INVALID_ARGUMENT;
+    if (!aligned16(sf) || (p0 && !aligned16(p0)) || (dp && !aligned16(dp)) ||
+        (reinterpret_cast<uintptr_t>(flow) & 7))
+        return SGM_ERR_INVALID_ARGUMENT;
+    sgm::CombineParams p{};
+    p.W = h->prm.width; p.H = h->prm.height; p.rule = h->prm.bilinear_rule; p.nquads = 1;
+    p.d0 = d0; p.d1 = d1; p.v0 = v0; p.v1 = v1; p.disp_stride = 0;
+    p.flow = flow; p.flow_valid = flow_valid;
+    if (cam) {
+        p.f = cam->f_px; p.B = cam->baseline_m; p.cx = cam->cx; p.cy = cam->cy;
+        p.fB = cam->f_px * cam->baseline_m;
+    }
+    p.sf = sf; p.p0 = want3d ? p0 : nullptr; p.dp = dp; p.valid_sf = valid_sf; p.valid_3d = valid_3d;
+    cudaError_t e = sgm::launch_combine(p, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) ++h->launches;
+    return from_cuda(e);
+}
+
+static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *images, int64_t pitch,
+                                  const float *flow, const uint8_t *flow_valid,
+                                  const sgm_camera *cam, const sgm_sceneflow_out *out,
+                                  cudaStream_t st) {
+    const int W = h->prm.width, H = h->prm.height;
+    const long long npx = h->npx;
+    const bool want3d = out->p0 || out->dp || out->valid_3d;
+    if (want3d && (!out->p0 || !out->dp || !out->valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
+    if (want3d && !(cam->f_px > 0.f && cam->baseline_m > 0.f)) return SGM_ERR_INVALID_ARGUMENT;
+    const bool timing = h->timing;
+    auto mark = [&](int i) {
+        if (timing) cudaEventRecord(h->ev[i], st);
+    };
+    mark(0);
+    cudaError_t e = sgm::launch_census_stack(images, (long long)H * pitch, 4 * n, pitch, W, H,
+                                             h->prm.census_w, h->prm.census_h, h->census, npx, st);
+    if (e != cudaSuccess) return from_cuda(e);
+    ++h->launches;
+    mark(1);
+    {
+        sgm::SweepParams p = sweep_params(h, 4 * n);
+        int nl = 0;
+        e = sgm::launch_sweeps(p, h->cpl, h->c64, h->nw, false, st, timing ? h->ev[2] : nullptr,
+                               nullptr, &nl);
+        h->launches += nl;
+        if (e != cudaSuccess) return from_cuda(e);
+    }
+    mark(3);
+    int16_t *di = out->disp_int ? out->disp_int : h->lr_int;
+    float *ds = out->disp_sub ? out->disp_sub : h->lr_sub;
+    uint8_t *dv = out->disp_valid ? out->disp_valid : h->lr_valid;
+    {
+        sgm::LrParams p{};
+        p.W = W; p.H = H; p.T = h->prm.lr_threshold; p.invalid = h->prm.invalid_disp;
+        p.npairs = 2 * n;
+        p.dl = h->dint; p.dls = h->dsub; p.dr = h->dint + npx;
+        p.in_stride_l = p.in_stride_r = 2 * npx;
+        p.out_int = di; p.out_sub = ds; p.valid = dv; p.out_stride = npx;
+        e = sgm::launch_lr(p, st);
+        if (e != cudaSuccess) return from_cuda(e);
+        ++h->launches;
+    }
+    mark(4);
+    {
+        sgm::CombineParams p{};
+        p.W = W; p.H = H; p.rule = h->prm.bilinear_rule; p.nquads = n;
+        p.d0 = ds; p.d1 = ds + npx; p.v0 = dv; p.v1 = dv + npx; p.disp_stride = 2 * npx;
+        p.flow = flow; p.flow_valid = flow_valid;
+        if (cam) {
+            p.f = cam->f_px; p.B = cam->baseline_m; p.cx = cam->cx; p.cy = cam->cy;
+            p.fB = cam->f_px * cam->baseline_m;
+        }
+        p.sf = out->sf; p.valid_sf = out->valid_sf;
+        p.p0 = want3d ? out->p0 : nullptr; p.dp = out->dp; p.valid_3d = out->valid_3d;
+        e = sgm::launch_combine(p, st);
+        if (e != cudaSuccess) return from_cuda(e);
+        ++h->launches;
+    }
+    mark(5);
+    if (timing) h->timed = true;
+    return SGM_OK;
+}
+
+sgm_status sgm_scene_flow(sgm_handle *h, int32_t n, const uint8_t *images, int64_t pitch_bytes,
+                          const float *flow, const uint8_t *flow_valid, const sgm_camera *cam,
+                          const sgm_sceneflow_out *out, void *stream) {
+    if (!h || !images || !flow || !out || !out->sf || !out->valid_sf) return SGM_ERR_INVALID_ARGUMENT;
+    if (n < 1 || n > h->prm.max_batch) return SGM_ERR_INVALID_ARGUMENT;
+    if (pitch_bytes < h->prm.width || (pitch_bytes % 16) != 0 || !aligned16(images) ||
+        !aligned16(out->sf) || (out->p0 && !aligned16(out->p0)) || (out->dp && !aligned16(out->dp)) ||
+        (reinterpret_cast<uintptr_t>(flow) & 7))
+        return SGM_ERR_INVALID_ARGUMENT;
+    return scene_flow_impl(h, n, images, pitch_bytes, flow, flow_valid, cam, out,
+                           static_cast<cudaStream_t>(stream));
+}
+
+sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, const float *flow,
+                               const uint8_t *flow_valid, const sgm_camera *cam,
+                               const sgm_sceneflow_out *out, void *stream) {
+    if (!h || !images || !flow || !out || !out->sf || !out->valid_sf) return SGM_ERR_INVALID_ARGUMENT;
+    if (n < 1 || n > h->prm.max_batch) return SGM_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int W = h->prm.width, H = h->prm.height;
+    const long long npx = h->npx;
+    cudaError_t e = cudaMemcpy2DAsync(h->img_stage, size_t(h->stage_pitch), images, size_t(W),
+                                      size_t(W), size_t(4LL * n * H), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h->flow_stage, flow, sizeof(float) * 2 * npx * n, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && flow_valid)
+        e = cudaMemcpyAsync(h->fvalid_stage, flow_valid, size_t(npx) * n, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return from_cuda(e);
+    sgm_sceneflow_out dev{};
+    dev.sf = h->sf_stage;
+    dev.valid_sf = h->vsf_stage;
+    const bool want3d = out->p0 || out->dp || out->valid_3d;
+    if (want3d) { dev.p0 = h->p0_stage; dev.dp = h->dp_stage; dev.valid_3d = h->v3_stage; }
+    const bool want_disp = out->disp_int || out->disp_sub || out->disp_valid;
+    sgm_status s = scene_flow_impl(h, n, h->img_stage, h->stage_pitch, h->flow_stage,
+                                   flow_valid ? h->fvalid_stage : nullptr, cam, &dev, st);
+    if (s != SGM_OK) return s;
+    auto d2h = [&](void *dst, const void *src, size_t bytes) {
+        if (dst && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+    };
+    d2h(out->sf, h->sf_stage, sizeof(float) * 4 * npx * n);
+    d2h(out->valid_sf, h->vsf_stage, size_t(npx) * n);
+    if (want3d) {
+        d2h(out->p0, h->p0_stage, sizeof(float) * 4 * npx * n);
+        d2h(out->dp, h->dp_stage, sizeof(float) * 4 * npx * n);
+        d2h(out->valid_3d, h->v3_stage, size_t(npx) * n);
+    }
+    if (want_disp) {
+        d2h(out->disp_int, h->lr_int, sizeof(int16_t) * 2 * npx * n);
+        d2h(out->disp_sub, h->lr_sub, sizeof(float) * 2 * npx * n);
+        d2h(out->disp_valid, h->lr_valid, size_t(2 * npx) * n);
+    }
+    return from_cuda(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,161 @@
+// census.cu -- census transform (G2-G4) with TMA-staged shared-memory tiles.
+//
+// out[y][x] bit k = [I(clamp(x+dx), clamp(y+dy)) < I(x, y)] for the k-th neighbour of the
+// census_w x census_h window scanned row-major (dy outer, dx inner), centre skipped.
+//
+// Each CTA owns a 64 x 16 output tile.  One elected thread issues a 3D
+// cp.async.bulk.tensor (TMA) for the tile plus its halo -- box {80, 16 + 2*ry, 1} of the
+// image stack [nimg][H][pitch] -- into shared memory, completing on an mbarrier with
+// expect_tx.  TMA fills out-of-image texels with zeros, not with the clamped border the
+// method needs, so every neighbour read goes through clamped image coordinates; the box
+// always contains the clamped texel (it spans [x0-rx, x0-rx+80) x [y0-ry, y0+16+ry)).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "sgm_internal.cuh"
+
+namespace sgm {
+namespace {
+
+constexpr int kTileW = 64;
+constexpr int kTileH = 16;
+constexpr int kBoxW = 80;          // >= kTileW + 2*rx for census_w <= 17, multiple of 16 B
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <int CW, int CH>
+__device__ __forceinline__ uint64_t census_px(const uint8_t *s, int bh, int gx, int gy, int ox,
+                                              int oy, int W, int H, int cw_rt, int ch_rt) {
+    const int cw = CW > 0 ? CW : cw_rt;
+    const int ch = CH > 0 ? CH : ch_rt;
+    const int rx = cw / 2, ry = ch / 2;
+    (void)bh;
+    const int c = s[(gy - oy) * kBoxW + (gx - ox)];
+    uint64_t bits = 0;
+    int k = 0;
+#pragma unroll
+    for (int dy = -ry; dy <= ry; ++dy) {
+        int yy = gy + dy;
+        yy = yy < 0 ? 0 : (yy > H - 1 ? H - 1 : yy);
+        const uint8_t *row = s + (yy - oy) * kBoxW;
+#pragma unroll
+        for (int dx = -rx; dx <= rx; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            int xx = gx + dx;
+            xx = xx < 0 ? 0 : (xx > W - 1 ? W - 1 : xx);
+            const int n = row[xx - ox];
+            bits |= uint64_t(n < c) << k;
+            ++k;
+        }
+    }
+    return bits;
+}
+
+template <int CW, int CH>
+__global__ void __launch_bounds__(kThreads) census_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                          CensusParams prm, uint64_t *out,
+                                                          long long out_stride) {
+    const int cw = CW > 0 ? CW : prm.cw;
+    const int ch = CH > 0 ? CH : prm.ch;
+    const int rx = cw / 2, ry = ch / 2;
+    const int bh = kTileH + 2 * ry;
+    __shared__ __align__(128) uint8_t tile[kBoxW * (kTileH + 2 * 8)];
+    __shared__ __align__(8) unsigned long long mbar;
+
+    const int x0 = blockIdx.x * kTileW, y0 = blockIdx.y * kTileH, img = blockIdx.z;
+    const int ox = x0 - rx, oy = y0 - ry;           // image coords of tile[0][0]
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const unsigned bytes = unsigned(kBoxW * bh);
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(&mbar)),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(tile)),
+            "l"(&tmap), "r"(ox), "r"(oy), "r"(img), "r"(smem_u32(&mbar))
+            : "memory");
+    }
+    __syncthreads();
+    {
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], 0;\n"
+                " selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(smem_u32(&mbar))
+                : "memory");
+        }
+    }
+    uint64_t *o = out + (long long)img * out_stride;
+    for (int k = threadIdx.x; k < kTileW * kTileH; k += kThreads) {
+        const int lx = k % kTileW, ly = k / kTileW;
+        const int gx = x0 + lx, gy = y0 + ly;
+        if (gx < prm.W && gy < prm.H)
+            o[(long long)gy * prm.W + gx] =
+                census_px<CW, CH>(tile, bh, gx, gy, ox, oy, prm.W, prm.H, cw, ch);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+// imgs: nimg images with a constant stride (img_stride bytes) starting at base.
+cudaError_t launch_census_stack(const uint8_t *base, long long img_stride, int nimg, long long pitch,
+                                int W, int H, int cw, int ch, uint64_t *out, long long out_stride,
+                                cudaStream_t st) {
+    auto enc = get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch & 15) || (img_stride & 15) || ch / 2 > 8 ||
+        cw / 2 > (kBoxW - kTileW) / 2)
+        return cudaErrorInvalidValue;
+    CUtensorMap tmap;
+    const int ry = ch / 2;
+    cuuint64_t dims[3] = {cuuint64_t(W), cuuint64_t(H), cuuint64_t(nimg)};
+    cuuint64_t strides[2] = {cuuint64_t(pitch), cuuint64_t(img_stride)};
+    cuuint32_t box[3] = {cuuint32_t(kBoxW), cuuint32_t(kTileH + 2 * ry), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t *>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    CensusParams prm{W, H, cw, ch, nimg};
+    dim3 grid((W + kTileW - 1) / kTileW, (H + kTileH - 1) / kTileH, nimg);
+    if (cw == 9 && ch == 7)
+        census_kernel<9, 7><<<grid, kThreads, 0, st>>>(tmap, prm, out, out_stride);
+    else if (cw == 5 && ch == 5)
+        census_kernel<5, 5><<<grid, kThreads, 0, st>>>(tmap, prm, out, out_stride);
+    else
+        census_kernel<0, 0><<<grid, kThreads, 0, st>>>(tmap, prm, out, out_stride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_census(const uint8_t *const *imgs, int nimg, long long pitch, int W, int H,
+                          int cw, int ch, uint64_t *out, long long out_stride, cudaStream_t st) {
+    // independent pointers: one launch per image
+    for (int i = 0; i < nimg; ++i) {
+        cudaError_t e = launch_census_stack(imgs[i], (long long)H * pitch, 1, pitch, W, H, cw, ch,
+                                            out + (long long)i * out_stride, out_stride, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace sgm

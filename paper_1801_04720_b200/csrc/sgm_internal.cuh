@@ -1,0 +1,81 @@
+// sgm_internal.cuh -- device-side building blocks shared by the sm_100a kernels
+// of libsgmsf.so.  Nothing here is shared with oracle/ (the CPU oracle).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sgm {
+
+// ----------------------------------------------------------------- constants
+constexpr int kWarp = 32;
+constexpr int kRing = 4;        // intra-CTA row->row handoff ring (positions)
+constexpr int kRing0 = 16;      // band-input ring of warp 0 (positions)
+constexpr int kLook = 8;        // band-input prefetch distance (positions)
+constexpr int kPublish = 4;     // band-output progress publication granularity
+constexpr uint32_t kSent = 0x7FFF7FFFu;   // "no neighbour" path cost (both halves)
+constexpr uint32_t kPadCost = 0x10001000u; // OR-ed into padded disparities d >= D
+
+// ----------------------------------------------------------------- kernel params
+struct SweepParams {
+    int W, H, D, Dp;
+    int P1, P2, cmax;
+    int nviews, nbands;
+    // census images [img][H][W]; batch views: view v -> pair v/2, side v%2
+    //   side 0: ref = img 2*(v/2), match = img 2*(v/2)+1, mirror 0 (left reference)
+    //   side 1: ref = img 2*(v/2)+1, match = img 2*(v/2), mirror 1 (right reference)
+    const uint64_t *cen;
+    long long cen_img_stride;
+    // explicit single-view mode (sgm_aggregate / sgm_disparity with user census)
+    int explicit_mode;
+    const uint64_t *ref0, *match0;
+    int mirror0;
+    // forward-sweep sum S_fwd [view][H][W][Dp] in view coordinates (mirrored for right views)
+    uint16_t *sfwd;
+    long long sfwd_view_stride;
+    // backward-sweep outputs
+    int16_t *dint;            // [view][H][W] raw WTA (original x)
+    float *dsub;              // [view][H][W]
+    long long disp_view_stride;
+    uint16_t *sout;           // debug: S [H][W][D] of view 0 (original x), or null
+    // inter-band handoff
+    uint16_t *gbuf;           // [view][band][W][3][Dp]
+    int *progress;            // [view][band]
+    int *ticket;              // CTA ticket counter (zeroed before launch)
+};
+
+struct CensusParams {
+    int W, H, cw, ch, nimg;
+};
+
+struct LrParams {
+    int W, H, T, invalid, npairs;
+    const int16_t *dl; const float *dls; const int16_t *dr;
+    long long in_stride_l, in_stride_r;   // elements between consecutive pairs
+    int16_t *out_int; float *out_sub; uint8_t *valid;
+    long long out_stride;
+};
+
+struct CombineParams {
+    int W, H, rule, nquads;
+    const float *d0, *d1; const uint8_t *v0, *v1;
+    long long disp_stride;                 // elements between quads for d0/d1/v0/v1
+    const float *flow; const uint8_t *flow_valid;
+    float f, B, cx, cy, fB;
+    float *sf, *p0, *dp; uint8_t *valid_sf, *valid_3d;
+};
+
+// ----------------------------------------------------------------- launchers (host)
+cudaError_t launch_census(const uint8_t *const *imgs, int nimg, long long pitch, int W, int H,
+                          int cw, int ch, uint64_t *out, long long out_stride, cudaStream_t st);
+cudaError_t launch_cost(const uint64_t *ref, const uint64_t *match, int W, int H, int D, int s,
+                        int cmax, uint8_t *cost, cudaStream_t st);
+cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool debug_s,
+                          cudaStream_t st, cudaEvent_t mid_ev_a, cudaEvent_t mid_ev_b,
+                          int *launches);
+cudaError_t launch_wta(const uint16_t *agg, int W, int H, int D, int16_t *dint, float *dsub,
+                       cudaStream_t st);
+cudaError_t launch_lr(const LrParams &p, cudaStream_t st);
+cudaError_t launch_combine(const CombineParams &p, cudaStream_t st);
+
+}  // namespace sgm

@@ -1,0 +1,79 @@
+"""Host-side checks of the C-ABI library (no GPU needed): it loads, exports every
+symbol include/sgmsf.h declares, and rejects invalid parameters synchronously
+before touching the device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1801_04720_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "sgmsf.h")).read()
+    return sorted(set(re.findall(r"^SGM_API[^(]*?\b(sgm_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_header_declares_documented_entry_points():
+    syms = header_symbols()
+    assert syms == sorted(_lib.EXPORTS)
+    for name in ("sgm_create", "sgm_census", "sgm_cost", "sgm_aggregate", "sgm_wta",
+                 "sgm_lr_check", "sgm_combine_sceneflow"):
+        assert name in syms          # BASELINE.json north_star's named calls
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+        assert ctypes.cast(getattr(lib, name), ctypes.c_void_p).value
+
+
+def test_status_strings():
+    lib = _lib.load()
+    for code in range(5):
+        s = lib.sgm_status_string(code)
+        assert s and s.decode()
+    assert lib.sgm_stage_name(0) == b"census" and lib.sgm_stage_name(99) == b"?"
+
+
+GOOD = dict(width=64, height=48, num_disp=16, census_w=5, census_h=5, p1=10, p2=120,
+            lr_threshold=1, invalid_disp=-1, bilinear_rule=0, max_batch=1)
+
+
+@pytest.mark.parametrize("field,value", [
+    ("width", 0), ("height", -1), ("num_disp", 0), ("num_disp", 257),
+    ("census_w", 4), ("census_h", 6), ("census_w", 11),          # 11*7-1 > 64 bits
+    ("p1", -1), ("p2", 5),                                       # P2 < P1 (G8)
+    ("p2", 240),                                                 # C_max + P2 > 255 (G9)
+    ("lr_threshold", -1), ("bilinear_rule", 2), ("max_batch", 0),
+])
+def test_create_rejects_invalid_params(field, value):
+    lib = _lib.load()
+    kw = dict(GOOD)
+    if field == "census_w" and value == 11:
+        kw["census_h"] = 7
+    kw[field] = value
+    p = _lib.SgmParams(**kw)
+    h = ctypes.c_void_p()
+    assert lib.sgm_create(ctypes.byref(p), 0, ctypes.byref(h)) == 1
+    assert h.value is None
+
+
+def test_null_handle_calls_are_rejected():
+    lib = _lib.load()
+    assert lib.sgm_census(None, None, 64, None, None) == 1
+    assert lib.sgm_scene_flow(None, 1, None, 64, None, None, None, None, None) == 1
+    assert lib.sgm_launch_count(None) == 0
+    lib.sgm_destroy(None)
+
+
+def test_no_fallback_when_library_missing(tmp_path, monkeypatch):
+    """The binding raises instead of silently computing anything else."""
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib._build, "NVCC", str(tmp_path / "no-nvcc"))
+    with pytest.raises(_lib.SgmLibraryError):
+        _lib.load(str(tmp_path / "libsgmsf.so"))
