@@ -102,6 +102,10 @@ SGM_API void sgm_destroy(sgm_handle *h);
 /* Static description of a status code (never NULL). */
 SGM_API const char *sgm_status_string(sgm_status s);
 
+/* Human-readable description of the most recent CUDA failure seen by this
+ * thread inside the library (e.g. "cudaErrorInvalidValue: invalid argument"). */
+SGM_API const char *sgm_last_error_string(void);
+
 /* Census transform of one uint8 image (G2-G4): out[y][x] bit k =
  * [neighbour k < centre] over the census_w x census_h window scanned row-major
  * (dy outer, dx inner), centre skipped, coordinates clamped to the image.

@@ -24,7 +24,7 @@ EXPORTS = (
     "sgm_create", "sgm_destroy", "sgm_status_string", "sgm_census", "sgm_cost", "sgm_aggregate",
     "sgm_wta", "sgm_lr_check", "sgm_disparity", "sgm_combine_sceneflow", "sgm_scene_flow",
     "sgm_scene_flow_host", "sgm_set_timing", "sgm_read_timing", "sgm_stage_name",
-    "sgm_launch_count", "sgm_get_geometry",
+    "sgm_launch_count", "sgm_get_geometry", "sgm_last_error_string",
 )
 
 
@@ -38,6 +38,8 @@ class SgmError(RuntimeError):
         if lib is not None:
             try:
                 msg += ": " + lib.sgm_status_string(code).decode()
+                if code == 3:
+                    msg += " (" + lib.sgm_last_error_string().decode() + ")"
             except Exception:  # pragma: no cover
                 pass
         super().__init__(f"{fn} failed: {msg}")
@@ -90,6 +92,7 @@ def load(path: str | None = None):
         "sgm_create": (st, [ctypes.POINTER(SgmParams), I32, ctypes.POINTER(P)]),
         "sgm_destroy": (None, [P]),
         "sgm_status_string": (ctypes.c_char_p, [st]),
+        "sgm_last_error_string": (ctypes.c_char_p, []),
         "sgm_census": (st, [P, P, I64, P, P]),
         "sgm_cost": (st, [P, P, P, I32, P, P]),
         "sgm_aggregate": (st, [P, P, P, I32, P, P]),

@@ -48,8 +48,11 @@ struct sgm_handle {
 
 namespace {
 
+thread_local char g_last_error[256] = "no error";
+
 sgm_status from_cuda(cudaError_t e) {
     if (e == cudaSuccess) return SGM_OK;
+    snprintf(g_last_error, sizeof(g_last_error), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
     if (e == cudaErrorMemoryAllocation) return SGM_ERR_OUT_OF_MEMORY;
     if (e == cudaErrorInvalidValue) return SGM_ERR_INVALID_ARGUMENT;
     return SGM_ERR_CUDA;
@@ -100,6 +103,8 @@ const char *sgm_status_string(sgm_status s) {
     }
     return "unknown status";
 }
+
+const char *sgm_last_error_string(void) { return g_last_error; }
 
 const char *sgm_stage_name(int32_t stage) {
     static const char *names[SGM_NUM_STAGES] = {"census", "sweep_fwd", "sweep_bwd_wta", "lr_check",

@@ -4,11 +4,13 @@
 // census_w x census_h window scanned row-major (dy outer, dx inner), centre skipped.
 //
 // Each CTA owns a 64 x 16 output tile.  One elected thread issues a 3D
-// cp.async.bulk.tensor (TMA) for the tile plus its halo -- box {80, 16 + 2*ry, 1} of the
+// cp.async.bulk.tensor (TMA) for the tile plus its halo -- box {96, 16 + 2*ry, 1} of the
 // image stack [nimg][H][pitch] -- into shared memory, completing on an mbarrier with
 // expect_tx.  TMA fills out-of-image texels with zeros, not with the clamped border the
 // method needs, so every neighbour read goes through clamped image coordinates; the box
-// always contains the clamped texel (it spans [x0-rx, x0-rx+80) x [y0-ry, y0+16+ry)).
+// always contains the clamped texel (it spans [x0-16, x0+80) x [y0-ry, y0+16+ry)).  The box
+// x origin is x0-16, not x0-rx: TMA requires the innermost start coordinate times the
+// element size to be a multiple of 16 bytes.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -19,7 +21,8 @@ namespace {
 
 constexpr int kTileW = 64;
 constexpr int kTileH = 16;
-constexpr int kBoxW = 80;          // >= kTileW + 2*rx for census_w <= 17, multiple of 16 B
+constexpr int kHaloX = 16;         // TMA box x origin must be 16-byte aligned: start at x0-16
+constexpr int kBoxW = kTileW + 2 * kHaloX;   // 96 bytes, covers rx <= 16
 constexpr int kThreads = 256;
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -60,13 +63,14 @@ __global__ void __launch_bounds__(kThreads) census_kernel(const __grid_constant_
                                                           long long out_stride) {
     const int cw = CW > 0 ? CW : prm.cw;
     const int ch = CH > 0 ? CH : prm.ch;
-    const int rx = cw / 2, ry = ch / 2;
+    (void)cw;
+    const int ry = ch / 2;
     const int bh = kTileH + 2 * ry;
     __shared__ __align__(128) uint8_t tile[kBoxW * (kTileH + 2 * 8)];
     __shared__ __align__(8) unsigned long long mbar;
 
     const int x0 = blockIdx.x * kTileW, y0 = blockIdx.y * kTileH, img = blockIdx.z;
-    const int ox = x0 - rx, oy = y0 - ry;           // image coords of tile[0][0]
+    const int ox = x0 - kHaloX, oy = y0 - ry;       // image coords of tile[0][0]
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -124,7 +128,7 @@ cudaError_t launch_census_stack(const uint8_t *base, long long img_stride, int n
     auto enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch & 15) || (img_stride & 15) || ch / 2 > 8 ||
-        cw / 2 > (kBoxW - kTileW) / 2)
+        cw / 2 > kHaloX)
         return cudaErrorInvalidValue;
     CUtensorMap tmap;
     const int ry = ch / 2;
