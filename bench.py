@@ -37,7 +37,7 @@ UNIT = "cells/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="batch", choices=["batch", "driving", "wide", "highres", "tiny"])
@@ -65,7 +65,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -227,7 +227,6 @@ def main():
     def step():
         sgm.scene_flow(imgs, flow, cam, out, stream=stream)
 
-    sgm.set_timing(True)
     graph = None
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
@@ -269,14 +268,23 @@ def main():
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
-            t = sgm.read_timing()
-            if t:
-                for k, v in t.items():
-                    stage_ms.setdefault(k, []).append(v)
     torch.cuda.synchronize(dev)
     if pg is not None:
         dist.barrier()
     clk = clocks.stop()
+    # per-kernel durations: the same steps launched eagerly with the library's CUDA events
+    # recorded on the launch stream around every kernel (graph replays cannot be split)
+    sgm.set_timing(True)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            flush.fill_(1)
+            step()
+            stream.synchronize()
+            t = sgm.read_timing()
+            if t:
+                for k, v in t.items():
+                    stage_ms.setdefault(k, []).append(v)
+    sgm.set_timing(False)
     total_ms = max_over_ranks(total_ms, dev)
     ms_per_step = total_ms / args.steps
     W, H, D = cfg.W, cfg.H, cfg.D
