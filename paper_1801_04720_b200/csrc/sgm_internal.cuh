@@ -9,7 +9,7 @@ namespace sgm {
 
 // ----------------------------------------------------------------- constants
 constexpr int kWarp = 32;
-constexpr int kRing = 4;        // intra-CTA row->row handoff ring (positions)
+constexpr int kRing = 8;        // intra-CTA row->row handoff ring (positions, mbarrier per slot)
 constexpr int kRing0 = 16;      // band-input ring of warp 0 (positions)
 constexpr int kLook = 8;        // band-input prefetch distance (positions)
 constexpr int kPublish = 4;     // band-output progress publication granularity

@@ -106,10 +106,11 @@ __device__ __forceinline__ void st_relaxed_gpu(int *p, int v) {
 
 // One semi-global path update for the CPL cells a lane holds.
 //   prev: L_r(p - r, .) (u16x2 pairs), C: C(p, .), out: L_r(p, .).
+//   sel_up / sel_dn: PRMT selectors building the d-1 / d+1 neighbour pairs (per lane).
 template <int R>
 __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uint32_t (&C)[R],
                                             uint32_t (&out)[R], uint32_t p1x2, uint32_t p2x2,
-                                            int lane) {
+                                            uint32_t sel_up, uint32_t sel_dn) {
     // m = min_k L_r(p - r, k), broadcast as m * 0x10001
     uint32_t v = prev[0];
 #pragma unroll
@@ -117,23 +118,20 @@ __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uin
     v = __vminu2(v, __byte_perm(v, 0, 0x1032));
     const uint32_t mm = __reduce_min_sync(0xffffffffu, v);
     const uint32_t mP2 = mm + p2x2;      // m + P2 in both halves
-    const uint32_t K = 0u - mm;          // adds -m to both halves (carry-exact)
     // neighbours d-1 / d+1
-    uint32_t up = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
-    uint32_t dn = __shfl_down_sync(0xffffffffu, prev[0], 1);
-    up = lane == 0 ? kSent : up;
-    dn = lane == 31 ? kSent : dn;
+    const uint32_t up = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
+    const uint32_t dn = __shfl_down_sync(0xffffffffu, prev[0], 1);
     uint32_t nb[R + 1];
-    nb[0] = __byte_perm(up, prev[0], 0x5432);
+    nb[0] = __byte_perm(up, prev[0], sel_up);
 #pragma unroll
     for (int r = 1; r < R; ++r) nb[r] = __byte_perm(prev[r - 1], prev[r], 0x5432);
-    nb[R] = __byte_perm(prev[R - 1], dn, 0x5432);
+    nb[R] = __byte_perm(prev[R - 1], dn, sel_dn);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         uint32_t t = __vminu2(nb[r], nb[r + 1]);       // min(L(d-1), L(d+1))
         t = __viaddmin_u16x2(t, p1x2, prev[r]);        // min(.. + P1, L(d))
         t = __vminu2(t, mP2);                          // min(.., m + P2)
-        out[r] = t + C[r] + K;                         // + C - m
+        out[r] = t + C[r] - mm;                        // + C - m (carry-exact)
     }
 }
 
@@ -151,9 +149,29 @@ struct Sweep {
         if (BWD) {
             b += size_t(NW) * DP * 2;               // WTA scratch
         }
+        b += size_t(2) * NW * kRing * 8;            // full / empty mbarriers
         return b;
     }
 };
+
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
 
 template <int CPL, bool C64, bool BWD, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) {
@@ -167,19 +185,34 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
     uint16_t *in0 = ring + size_t(NW) * kRing * VEC;
     uint64_t *cbuf = reinterpret_cast<uint64_t *>(in0 + size_t(kRing0) * VEC);
     uint16_t *wsc = reinterpret_cast<uint16_t *>(cbuf + size_t(NW) * 2 * 64);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(wsc + (BWD ? size_t(NW) * DP : 0));
+    // full[w][s]: slot s of warp w's ring holds complete data (32 producer lanes arrive)
+    // empty[w][s]: the consumer (warp w+1) is done with slot s (32 consumer lanes arrive)
 
+    // Zero the path-vector rings: a zero vector with m = 0 makes the recursion return
+    // L = C, i.e. every slot nobody writes acts as a path start.
+    {
+        uint4 *z = reinterpret_cast<uint4 *>(smem_raw);
+        const int n16 = int((size_t(NW) * kRing + kRing0) * VEC * 2 / 16);
+        for (int k = threadIdx.x; k < n16; k += NW * 32) z[k] = make_uint4(0u, 0u, 0u, 0u);
+    }
     __shared__ int s_ticket;
+    if (threadIdx.x < 2 * NW * kRing) mbar_init(bars + threadIdx.x, 32);
     if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
     const int ticket = s_ticket;
     const int band = ticket / p.nviews;
     const int view = ticket - band * p.nviews;
 
-    const int warp = threadIdx.x >> 5;
+    // warp index through a warp reduction: the compiler then keeps it (and everything
+    // derived from it) in uniform registers and emits uniform branches.
+    const int warp = int(__reduce_min_sync(0xffffffffu, threadIdx.x >> 5));
     const int lane = lane_id();
     const int W = p.W, H = p.H;
     const int j = band * NW + warp;                 // iteration row
-    const bool row_ok = j < H;
+    if (j >= H) return;                             // rows past the image (last band)
+    const bool has_row_below = (warp < NW - 1) && (j + 1 < H);
     const int y = BWD ? (H - 1 - j) : j;
 
     const uint64_t *ref, *match;
@@ -194,17 +227,25 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
         match = side ? a : b;
         mirror = side;
     }
-    const long long yrow = (long long)(row_ok ? y : 0) * W;
+    const long long yrow = (long long)y * W;
     const uint64_t *ref_row = ref + yrow;
     const uint64_t *match_row = match + yrow;
-    uint16_t *sfwd_row = p.sfwd + (long long)view * p.sfwd_view_stride + yrow * DP;
     auto X = [&](int xv) { return mirror ? (W - 1 - xv) : xv; };   // view x' -> image x
     auto xview = [&](int i) { return BWD ? (W - 1 - i) : i; };      // iteration i -> x'
+    // S_fwd row in view coordinates; the backward sweep walks it from the right end
+    uint16_t *sfwd_row = p.sfwd + (long long)view * p.sfwd_view_stride + yrow * DP + CPL * lane;
+    const long long sstep = BWD ? -DP : DP;
+    uint16_t *sfwd_ptr = sfwd_row + (BWD ? (long long)(W - 1) * DP : 0);
 
     // per-lane constants
     const uint32_t p1x2 = uint32_t(p.P1) * 0x10001u;
     const uint32_t p2x2 = uint32_t(p.P2) * 0x10001u;
     const int dbase = CPL * lane;
+    // PRMT selectors for the d-1 / d+1 neighbour pairs: at d = 0 (lane 0) the missing d-1
+    // candidate is replaced by the d+1 one (min(L(1), L(1)) == min over existing terms,
+    // G7) and symmetrically at d = Dp-1 (lane 31).
+    const uint32_t sel_up = lane == 0 ? 0x5476u : 0x5432u;
+    const uint32_t sel_dn = lane == 31 ? 0x1032u : 0x5432u;
     uint32_t pad[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -214,33 +255,42 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
 #pragma unroll
     for (int r = 0; r < R; ++r) dcode[r] = uint32_t(dbase + 2 * r) | (uint32_t(dbase + 2 * r + 1) << 8);
 
-    // shared-memory views of this warp
-    uint16_t *my_ring = ring + size_t(warp) * kRing * VEC;
-    const uint16_t *src_ring = warp == 0 ? in0 : ring + size_t(warp - 1) * kRing * VEC;
-    const int src_mask = warp == 0 ? (kRing0 - 1) : (kRing - 1);
-    const bool have_above = j > 0;                  // row j-1 exists in the view
+    // Ring layout (consumer-centric): slot s of a warp's ring holds, for the position q
+    // with q & (kRing-1) == s, the three row-above vectors the consumer needs at q:
+    //   v0 = L_down(q), v1 = L_diag(q-1) (predecessor of the (1,1) path),
+    //   v2 = L_anti(q+1) (predecessor of the (-1,1) path).
+    // The producer at position p writes v0 -> slot p, v1 -> slot p+1, v2 -> slot p-1, and
+    // arrives on full[p-1] (its v2 is the last write into that slot).
+    uint16_t *my_ring = ring + size_t(warp) * kRing * VEC + dbase;
+    const uint16_t *src_ring = (warp == 0 ? in0 : ring + size_t(warp - 1) * kRing * VEC) + dbase;
+    uint64_t *my_full = bars + size_t(warp) * kRing;
+    uint64_t *my_empty = bars + size_t(NW + warp) * kRing;           // released by warp+1
+    uint64_t *src_full = bars + size_t(warp - 1) * kRing;            // (warp >= 1)
+    uint64_t *src_empty = bars + size_t(NW + warp - 1) * kRing;
     uint64_t *cref = cbuf + size_t(warp) * 128;
     uint64_t *cfresh = cref + 64;
     uint16_t *wta = wsc + size_t(warp) * DP;
 
-    // band handoff
+    // band handoff (gbuf row has the same consumer-centric layout per position)
     const int nb_id = view * p.nbands + band;
     const bool has_consumer = band + 1 < p.nbands;
     const bool is_producer = (warp == NW - 1) && has_consumer;
-    uint16_t *gout = p.gbuf + (long long)nb_id * W * VEC;
+    uint16_t *gout = p.gbuf + (long long)nb_id * W * VEC + dbase;
     const uint16_t *gin = p.gbuf + (long long)(nb_id - 1) * W * VEC;
     int *prog_out = p.progress + nb_id;
     const int *prog_in = p.progress + (nb_id - 1);
     const bool band_input = (warp == 0) && band > 0;
+    const bool ring_input = warp > 0;
     int known = 0;                                  // producer progress seen (warp 0)
     constexpr int kChunks = VEC * 2 / 16;           // 16-byte chunks per position
 
-    auto issue_input = [&](int q) {                 // cp.async position q of the row above
+    auto issue_input = [&](int q) {                 // cp.async gbuf[q] -> in0 slot q
         if (q < W) {
-            if (known < q + 1) {
+            const int need = min(q + 2, W);
+            if (known < need) {
                 int k, spins = 0;
                 // bounded wait: a logic error must not hang the GPU (~>2 s of polling)
-                while ((k = ld_acquire_gpu(prog_in)) < q + 1 && ++spins < (1 << 25)) __nanosleep(64);
+                while ((k = ld_acquire_gpu(prog_in)) < need && ++spins < (1 << 25)) __nanosleep(64);
                 known = k;
             }
             const char *g = reinterpret_cast<const char *>(gin + (long long)q * VEC);
@@ -252,19 +302,15 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
     };
 
     // census prefetch: positions 0..63
-    auto census_fill = [&](int i0, int n) {
-        for (int k = lane; k < n; k += 32) {
-            const int i = i0 + k;
-            if (i < W) {
-                const int xv = xview(i);
-                int xm = xv - (BWD ? DP - 1 : 0);
-                xm = xm < 0 ? 0 : xm;
-                cref[i & 63] = __ldg(ref_row + X(xv));
-                cfresh[i & 63] = __ldg(match_row + X(xm));
-            }
+    for (int k = lane; k < 64; k += 32) {
+        if (k < W) {
+            const int xv = xview(k);
+            int xm = xv - (BWD ? DP - 1 : 0);
+            xm = xm < 0 ? 0 : xm;
+            cref[k] = __ldg(ref_row + X(xv));
+            cfresh[k] = __ldg(match_row + X(xm));
         }
-    };
-    if (row_ok) census_fill(0, 64);
+    }
     uint64_t stage_ref = 0, stage_fresh = 0;
 
     if (band_input) {
@@ -280,195 +326,219 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
     CW win[CPL];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) win[k] = 0;
+    if (BWD) {
+        // logical window before the first rotation: cm(W - d) (see the slide below)
+#pragma unroll
+        for (int jj = 0; jj < CPL; ++jj) {
+            int xm = W - (dbase + jj);
+            xm = xm < 0 ? 0 : (xm > W - 1 ? W - 1 : xm);
+            win[(jj + CPL - 1) % CPL] = CW(__ldg(match_row + X(xm)));
+        }
+    }
     uint32_t pf[2][R];                               // BWD: S_fwd prefetch (2 positions)
 #pragma unroll
     for (int r = 0; r < R; ++r) { pf[0][r] = 0; pf[1][r] = 0; }
-    if (BWD && row_ok) {
-        VecIO<R>::ld(sfwd_row + (long long)xview(0) * DP + dbase, pf[0]);
-        if (W > 1) VecIO<R>::ld(sfwd_row + (long long)xview(1) * DP + dbase, pf[1]);
+    if (BWD) {
+        VecIO<R>::ld(sfwd_ptr, pf[0]);
+        if (W > 1) VecIO<R>::ld(sfwd_ptr + sstep, pf[1]);
     }
-    int od = 0;
-    float os = 0.f;
+    uint32_t rec_key = 0, rec_ac = 0;                // BWD: WTA record of position (i & ~31) + lane
     const bool do_wta = BWD && p.dint != nullptr;
     const bool do_sout = BWD && p.sout != nullptr;
     int16_t *dint_row = do_wta ? p.dint + (long long)view * p.disp_view_stride + yrow : nullptr;
     float *dsub_row = do_wta ? p.dsub + (long long)view * p.disp_view_stride + yrow : nullptr;
-
+    const int Dm1 = p.D - 1;
     __syncwarp();
-    __syncthreads();
 
-    const int T = W + 2 * (NW - 1);
 #pragma unroll 1
-    for (int t0 = 0; t0 < T; t0 += CPL) {
+    for (int i0 = 0; i0 < W; i0 += CPL) {
 #pragma unroll
         for (int ph = 0; ph < CPL; ++ph) {
-            const int t = t0 + ph;
-            const int i = t - 2 * warp;
-            const bool active = row_ok && i >= 0 && i < W;
-
+            const int i = i0 + ph;
+            if (i >= W) break;
+            const int xv = xview(i);
             // --- band output publication (producer warp, before this step's stores)
-            if (is_producer) {
-                const int c = t - 2 * (NW - 1);
-                if (c >= 1 && c <= W && ((c % kPublish) == 0 || c == W)) {
-                    __threadfence();
-                    if (lane == 0) st_relaxed_gpu(prog_out, c);
-                }
+            if (is_producer && i > 0 && ((i % kPublish) == 0)) {
+                __threadfence();
+                if (lane == 0) st_relaxed_gpu(prog_out, i);
             }
-            if (active) {
-                const int xv = xview(i);
-                // --- band input: keep cp.async kLook positions ahead
-                if (band_input) {
-                    issue_input(i + kLook);
-                    cp_async_wait<kLook - 1>();
-                    __syncwarp();
+            // --- inputs of the row above
+            if (band_input) {
+                issue_input(i + kLook);
+                cp_async_wait<kLook>();
+                __syncwarp();
+            } else if (ring_input) {
+                mbar_wait(src_full + (i & (kRing - 1)), unsigned(i / kRing) & 1u);
+            }
+            // --- census prefetch refill
+            if ((i & 31) == 0) {
+                const int q = i + 32 + lane;
+                if (q < W) {
+                    const int xq = xview(q);
+                    int xm = xq - (BWD ? DP - 1 : 0);
+                    xm = xm < 0 ? 0 : xm;
+                    stage_ref = __ldg(ref_row + X(xq));
+                    stage_fresh = __ldg(match_row + X(xm));
                 }
-                // --- census prefetch refill
-                if ((i & 31) == 0) {
-                    const int q = i + 32 + lane;
-                    if (q < W) {
-                        const int xq = xview(q);
-                        int xm = xq - (BWD ? DP - 1 : 0);
-                        xm = xm < 0 ? 0 : xm;
-                        stage_ref = __ldg(ref_row + X(xq));
-                        stage_fresh = __ldg(match_row + X(xm));
-                    }
-                } else if ((i & 31) == 16) {
-                    const int q = i + 16 + lane;
-                    if (q < W) {
-                        cref[q & 63] = stage_ref;
-                        cfresh[q & 63] = stage_fresh;
-                    }
-                    __syncwarp();
+            } else if ((i & 31) == 16) {
+                const int q = i + 16 + lane;
+                if (q < W) {
+                    cref[q & 63] = stage_ref;
+                    cfresh[q & 63] = stage_fresh;
                 }
-                // --- BWD window initialisation (logical j <-> cm(W - d) before rotation)
-                if (BWD && i == 0) {
-#pragma unroll
-                    for (int jj = 0; jj < CPL; ++jj) {
-                        int xm = W - (dbase + jj);
-                        xm = xm < 0 ? 0 : (xm > W - 1 ? W - 1 : xm);
-                        const uint64_t v = __ldg(match_row + X(xm));
-                        win[(jj + ph - 1 + CPL) % CPL] = CW(v);
-                    }
-                }
-                // --- slide the census window by one position
-                {
-                    const uint64_t fresh = cfresh[i & 63];
-                    if (!BWD) {
-                        const int q = (CPL - ph) % CPL;       // outgoing logical CPL-1
-                        CW v = __shfl_up_sync(0xffffffffu, win[q], 1);
-                        win[q] = lane == 0 ? CW(fresh) : v;
-                    } else {
-                        const int q = (ph - 1 + CPL) % CPL;   // outgoing logical 0
-                        CW v = __shfl_down_sync(0xffffffffu, win[q], 1);
-                        win[q] = lane == 31 ? CW(fresh) : v;
-                    }
-                }
-                // --- matching cost C(x', d) for the lane's CPL cells
-                uint32_t C[R];
-                {
-                    const uint64_t rv = cref[i & 63];
-                    uint32_t c[CPL];
-#pragma unroll
-                    for (int jj = 0; jj < CPL; ++jj) {
-                        const int phys = BWD ? (jj + ph) % CPL : (jj - ph + CPL) % CPL;
-                        if (C64) c[jj] = __popcll(rv ^ uint64_t(win[phys]));
-                        else c[jj] = __popc(uint32_t(rv) ^ uint32_t(win[phys]));
-                    }
-                    if (xv < p.D - 1) {                        // border: x' - d < 0 -> C_max
-#pragma unroll
-                        for (int jj = 0; jj < CPL; ++jj)
-                            if (dbase + jj > xv) c[jj] = uint32_t(p.cmax);
-                    }
-#pragma unroll
-                    for (int r = 0; r < R; ++r) C[r] = __byte_perm(c[2 * r], c[2 * r + 1], 0x5410) | pad[r];
-                }
-                // --- horizontal path (registers)
-                uint32_t S[R];
-                {
-                    uint32_t nL[R];
-                    path_update<R>(Lh, C, nL, p1x2, p2x2, lane);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) { Lh[r] = nL[r]; S[r] = nL[r]; }
-                }
-                // --- vertical + diagonal paths from the row above
-                uint16_t *dst = nullptr;
-                if (warp < NW - 1) dst = my_ring + size_t(i & (kRing - 1)) * VEC;
-                else if (is_producer) dst = gout + (long long)i * VEC;
-#pragma unroll
-                for (int v = 0; v < 3; ++v) {
-                    // v = 0: down (row above at i), 1: diagonal from (i-1), 2: diagonal from (i+1)
-                    const int q = i + (v == 1 ? -1 : (v == 2 ? 1 : 0));
-                    uint32_t prev[R];
-                    if (have_above && q >= 0 && q < W) {
-                        VecIO<R>::ld(src_ring + size_t(q & src_mask) * VEC + v * DP + dbase, prev);
-                    } else {
-#pragma unroll
-                        for (int r = 0; r < R; ++r) prev[r] = 0;
-                    }
-                    uint32_t nL[R];
-                    path_update<R>(prev, C, nL, p1x2, p2x2, lane);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) S[r] += nL[r];
-                    if (dst) VecIO<R>::st(dst + v * DP + dbase, nL);
-                }
-                // --- sweep output
+                __syncwarp();
+            }
+            // --- slide the census window by one position
+            {
+                const uint64_t fresh = cfresh[i & 63];
                 if (!BWD) {
-                    VecIO<R>::st(sfwd_row + (long long)xv * DP + dbase, S);
+                    const int q = (CPL - ph) % CPL;       // outgoing logical CPL-1
+                    CW v = __shfl_up_sync(0xffffffffu, win[q], 1);
+                    win[q] = lane == 0 ? CW(fresh) : v;
                 } else {
-                    uint32_t St[R];
-                    const int slot = ph & 1;
+                    const int q = (ph - 1 + CPL) % CPL;   // outgoing logical 0
+                    CW v = __shfl_down_sync(0xffffffffu, win[q], 1);
+                    win[q] = lane == 31 ? CW(fresh) : v;
+                }
+            }
+            // --- matching cost C(x', d) for the lane's CPL cells
+            uint32_t C[R];
+            {
+                const uint64_t rv = cref[i & 63];
+                uint32_t c[CPL];
 #pragma unroll
-                    for (int r = 0; r < R; ++r) St[r] = S[r] + pf[slot][r];
-                    if (i + 2 < W) VecIO<R>::ld(sfwd_row + (long long)xview(i + 2) * DP + dbase, pf[slot]);
+                for (int jj = 0; jj < CPL; ++jj) {
+                    const int phys = BWD ? (jj + ph) % CPL : (jj - ph + CPL) % CPL;
+                    if (C64) c[jj] = __popcll(rv ^ uint64_t(win[phys]));
+                    else c[jj] = __popc(uint32_t(rv) ^ uint32_t(win[phys]));
+                }
+                if (xv < Dm1) {                            // border: x' - d < 0 -> C_max
+#pragma unroll
+                    for (int jj = 0; jj < CPL; ++jj)
+                        if (dbase + jj > xv) c[jj] = uint32_t(p.cmax);
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) C[r] = __byte_perm(c[2 * r], c[2 * r + 1], 0x5410) | pad[r];
+            }
+            // --- row-above predecessors: all three live in slot i
+            uint32_t pv[3][R];
+            {
+                const uint16_t *src = src_ring + size_t(i & (band_input || warp == 0 ? kRing0 - 1 : kRing - 1)) * VEC;
+#pragma unroll
+                for (int v = 0; v < 3; ++v) VecIO<R>::ld(src + v * DP, pv[v]);
+            }
+            if (ring_input) {
+                __syncwarp();
+                mbar_arrive(src_empty + (i & (kRing - 1)));
+            }
+            // --- the four path updates (->, down, two diagonals)
+            uint32_t S[R];
+            {
+                uint32_t nL[R];
+                path_update<R>(Lh, C, nL, p1x2, p2x2, sel_up, sel_dn);
+#pragma unroll
+                for (int r = 0; r < R; ++r) { Lh[r] = nL[r]; S[r] = nL[r]; }
+            }
+            uint32_t nv[3][R];
+#pragma unroll
+            for (int v = 0; v < 3; ++v) {
+                path_update<R>(pv[v], C, nv[v], p1x2, p2x2, sel_up, sel_dn);
+#pragma unroll
+                for (int r = 0; r < R; ++r) S[r] += nv[v][r];
+            }
+            // --- hand the three vectors to the row below
+            if (has_row_below) {
+                if (i + 1 - kRing >= 0)                   // slot i+1 free again?
+                    mbar_wait(my_empty + ((i + 1) & (kRing - 1)), unsigned((i + 1) / kRing - 1) & 1u);
+                VecIO<R>::st(my_ring + size_t(i & (kRing - 1)) * VEC, nv[0]);
+                VecIO<R>::st(my_ring + size_t((i + 1) & (kRing - 1)) * VEC + DP, nv[1]);
+                VecIO<R>::st(my_ring + size_t((i - 1) & (kRing - 1)) * VEC + 2 * DP, nv[2]);
+                if (i > 0) mbar_arrive(my_full + ((i - 1) & (kRing - 1)));
+            } else if (is_producer) {
+                uint16_t *g = gout + (long long)i * VEC;
+                uint32_t zero[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) zero[r] = 0;
+                VecIO<R>::st(g, nv[0]);
+                if (i + 1 < W) VecIO<R>::st(g + VEC + DP, nv[1]);
+                if (i > 0) VecIO<R>::st(g - VEC + 2 * DP, nv[2]);
+                if (i == 0) VecIO<R>::st(g + DP, zero);            // no (i-1) predecessor
+                if (i == W - 1) VecIO<R>::st(g + 2 * DP, zero);    // no (i+1) predecessor
+            }
+            // --- sweep output
+            if (!BWD) {
+                VecIO<R>::st(sfwd_ptr, S);
+                sfwd_ptr += sstep;
+            } else {
+                uint32_t St[R];
+                const int slot = ph & 1;
+#pragma unroll
+                for (int r = 0; r < R; ++r) St[r] = S[r] + pf[slot][r];
+                if (i + 2 < W) VecIO<R>::ld(sfwd_ptr + 2 * sstep, pf[slot]);
+                sfwd_ptr += sstep;
+                if (do_sout) {
                     const int x = X(xv);
-                    if (do_sout) {
 #pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            const int d0 = dbase + 2 * r;
-                            uint16_t *o = p.sout + ((long long)y * W + x) * p.D;
-                            if (d0 < p.D) o[d0] = uint16_t(St[r] & 0xffffu);
-                            if (d0 + 1 < p.D) o[d0 + 1] = uint16_t(St[r] >> 16);
-                        }
+                    for (int r = 0; r < R; ++r) {
+                        const int d0 = dbase + 2 * r;
+                        uint16_t *o = p.sout + ((long long)y * W + x) * p.D;
+                        if (d0 < p.D) o[d0] = uint16_t(St[r] & 0xffffu);
+                        if (d0 + 1 < p.D) o[d0 + 1] = uint16_t(St[r] >> 16);
                     }
-                    if (do_wta) {
-                        uint32_t best = 0xffffffffu;
+                }
+                if (do_wta) {
+                    // smallest-index argmin via min of (S << 8 | d) (G10)
+                    uint32_t best = 0xffffffffu;
 #pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            const uint32_t k0 = __byte_perm(St[r], dcode[r], 0x6104);
-                            const uint32_t k1 = __byte_perm(St[r], dcode[r], 0x7325);
-                            best = min(best, min(k0, k1));
-                        }
-                        const uint32_t bkey = __reduce_min_sync(0xffffffffu, best);
-                        const int dstar = int(bkey & 0xffu);
-                        const int sb = int(bkey >> 8);
-                        VecIO<R>::st(wta + dbase, St);
-                        __syncwarp();
-                        float sub = float(dstar);
-                        if (dstar > 0 && dstar < p.D - 1) {
-                            const int sa = wta[dstar - 1];
-                            const int sc = wta[dstar + 1];
-                            const int den = 2 * (sa + sc - 2 * sb);
-                            float off = 0.f;
-                            if (den != 0) off = __fdiv_rn(float(sa - sc), float(den));
-                            off = fminf(fmaxf(off, -0.5f), 0.5f);
-                            sub = __fadd_rn(float(dstar), off);
-                        }
-                        __syncwarp();
-                        const int sl = i & 31;
-                        if (lane == sl) { od = dstar; os = sub; }
-                        if (sl == 31 || i == W - 1) {
-                            const int pos = (i & ~31) + lane;
-                            if (lane <= sl) {
-                                const int xo = X(xview(pos));
-                                dint_row[xo] = int16_t(od);
-                                dsub_row[xo] = os;
+                    for (int r = 0; r < R; ++r) {
+                        const uint32_t k0 = __byte_perm(St[r], dcode[r], 0x6104);
+                        const uint32_t k1 = __byte_perm(St[r], dcode[r], 0x7325);
+                        best = min(best, min(k0, k1));
+                    }
+                    const uint32_t bkey = __reduce_min_sync(0xffffffffu, best);
+                    const int dstar = int(bkey & 0xffu);
+                    __syncwarp();                                // previous reads of wta done
+                    VecIO<R>::st(wta + dbase, St);
+                    __syncwarp();
+                    const uint32_t sa = wta[max(dstar - 1, 0)];
+                    const uint32_t sc = wta[min(dstar + 1, DP - 1)];
+                    const int sl = i & 31;
+                    if (lane == sl) { rec_key = bkey; rec_ac = sa | (sc << 16); }
+                    // every 32 positions each lane finishes one pixel: the parabola
+                    // sub-pixel (one IEEE division per lane) and the stores
+                    if (sl == 31 || i == W - 1) {
+                        if (lane <= sl) {
+                            const int d = int(rec_key & 0xffu);
+                            const int b = int(rec_key >> 8);
+                            const int a = int(rec_ac & 0xffffu), c = int(rec_ac >> 16);
+                            float sub = float(d);
+                            if (d > 0 && d < Dm1) {
+                                const int den = 2 * (a + c - 2 * b);
+                                float off = 0.f;
+                                if (den != 0) off = __fdiv_rn(float(a - c), float(den));
+                                off = fminf(fmaxf(off, -0.5f), 0.5f);
+                                sub = __fadd_rn(float(d), off);
                             }
+                            const int xo = X(xview((i & ~31) + lane));
+                            dint_row[xo] = int16_t(d);
+                            dsub_row[xo] = sub;
                         }
                     }
                 }
             }
-            __syncthreads();
         }
+    }
+    if (has_row_below) {
+        // position W lies outside the image: the (-1,1) path of the row below starts at
+        // x' = W-1, so that slot's v2 must read as zero; then release slot W-1.
+        uint32_t zero[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) zero[r] = 0;
+        const int i = W;
+        if (i + 1 - kRing >= 0)
+            mbar_wait(my_empty + ((i + 1) & (kRing - 1)), unsigned((i + 1) / kRing - 1) & 1u);
+        VecIO<R>::st(my_ring + size_t((W - 1) & (kRing - 1)) * VEC + 2 * DP, zero);
+        mbar_arrive(my_full + ((W - 1) & (kRing - 1)));
     }
     if (is_producer) {
         __threadfence();
