@@ -217,6 +217,12 @@ SGM_API int64_t sgm_launch_count(sgm_handle *h);
 SGM_API sgm_status sgm_get_geometry(sgm_handle *h, int32_t *dp, int32_t *cells_per_lane,
                             int32_t *sweep_warps, int32_t *band_rows);
 
+/* Debugging aid: when `trace` (device memory, >= 4 * (sweep_warps + 1) * 4 * max_batch *
+ * ceil(H / band_rows) uint64) is non-NULL, every sweep CTA warp writes {start ns, end ns,
+ * SM id, 0} of its row loop at index (ticket * (sweep_warps + 1) + warp) * 4 (the last
+ * launch wins).  NULL disables it (default). */
+SGM_API sgm_status sgm_debug_set_trace(sgm_handle *h, uint64_t *trace);
+
 #ifdef __cplusplus
 }
 #endif

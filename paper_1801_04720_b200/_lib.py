@@ -24,7 +24,7 @@ EXPORTS = (
     "sgm_create", "sgm_destroy", "sgm_status_string", "sgm_census", "sgm_cost", "sgm_aggregate",
     "sgm_wta", "sgm_lr_check", "sgm_disparity", "sgm_combine_sceneflow", "sgm_scene_flow",
     "sgm_scene_flow_host", "sgm_set_timing", "sgm_read_timing", "sgm_stage_name",
-    "sgm_launch_count", "sgm_get_geometry", "sgm_last_error_string",
+    "sgm_launch_count", "sgm_get_geometry", "sgm_last_error_string", "sgm_debug_set_trace",
 )
 
 
@@ -109,6 +109,7 @@ def load(path: str | None = None):
         "sgm_read_timing": (I32, [P, ctypes.POINTER(ctypes.c_float)]),
         "sgm_stage_name": (ctypes.c_char_p, [I32]),
         "sgm_launch_count": (I64, [P]),
+        "sgm_debug_set_trace": (st, [P, P]),
         "sgm_get_geometry": (st, [P, ctypes.POINTER(I32), ctypes.POINTER(I32),
                                   ctypes.POINTER(I32), ctypes.POINTER(I32)]),
     }

@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libsgmsf.so (include/sgmsf.h): handle, validation, scratch,
 // launch orchestration on the caller's stream, status codes, instrumentation.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -44,6 +45,7 @@ struct sgm_handle {
     bool timed = false;
     cudaEvent_t ev[SGM_NUM_STAGES + 1] = {};
     long long launches = 0;
+    unsigned long long *trace = nullptr;   // debug timeline buffer (caller-owned, device)
 };
 
 namespace {
@@ -84,6 +86,12 @@ sgm::SweepParams sweep_params(const sgm_handle *h, int nviews) {
     p.dint = h->dint; p.dsub = h->dsub; p.disp_view_stride = h->npx;
     p.sout = nullptr;
     p.gbuf = h->gbuf; p.progress = h->sync + 1; p.ticket = h->sync;
+    p.trace = h->trace;
+    static const int dbg = [] {
+        const char *e = getenv("SGM_DEBUG_FLAGS");
+        return e ? atoi(e) : 0;
+    }();
+    p.debug_flags = dbg;
     return p;
 }
 
@@ -190,6 +198,12 @@ sgm_status sgm_get_geometry(sgm_handle *h, int32_t *dp, int32_t *cells_per_lane,
 }
 
 int64_t sgm_launch_count(sgm_handle *h) { return h ? h->launches : 0; }
+
+sgm_status sgm_debug_set_trace(sgm_handle *h, uint64_t *trace) {
+    if (!h) return SGM_ERR_INVALID_ARGUMENT;
+    h->trace = reinterpret_cast<unsigned long long *>(trace);
+    return SGM_OK;
+}
 
 sgm_status sgm_set_timing(sgm_handle *h, int32_t enable) {
     if (!h) return SGM_ERR_INVALID_ARGUMENT;

@@ -12,7 +12,8 @@ constexpr int kWarp = 32;
 constexpr int kRing = 8;        // intra-CTA row->row handoff ring (positions, mbarrier per slot)
 constexpr int kRing0 = 16;      // band-input ring of warp 0 (positions)
 constexpr int kLook = 8;        // band-input prefetch distance (positions)
-constexpr int kPublish = 4;     // band-output progress publication granularity
+constexpr int kPublish = 8;     // band-output progress publication granularity (positions)
+constexpr int kPubDepth = 4;    // producer -> publisher-warp handoff depth (groups)
 constexpr uint32_t kSent = 0x7FFF7FFFu;   // "no neighbour" path cost (both halves)
 constexpr uint32_t kPadCost = 0x10001000u; // OR-ed into padded disparities d >= D
 
@@ -42,6 +43,8 @@ struct SweepParams {
     uint16_t *gbuf;           // [view][band][W][3][Dp]
     int *progress;            // [view][band]
     int *ticket;              // CTA ticket counter (zeroed before launch)
+    unsigned long long *trace; // debug: per (ticket, warp) {start ns, end ns, smid, 0} or null
+    int debug_flags;           // debug (env SGM_DEBUG_FLAGS): 1 = no inter-warp/band waits
 };
 
 struct CensusParams {

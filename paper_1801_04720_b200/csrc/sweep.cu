@@ -100,6 +100,11 @@ __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_relaxed_gpu(int *p, int v) {
     asm volatile("st.relaxed.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
@@ -150,6 +155,7 @@ struct Sweep {
             b += size_t(NW) * DP * 2;               // WTA scratch
         }
         b += size_t(2) * NW * kRing * 8;            // full / empty mbarriers
+        b += size_t(2) * kPubDepth * 8;             // publisher mbarriers
         return b;
     }
 };
@@ -163,18 +169,21 @@ __device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(b)) : "memory");
 }
+// A waiting warp suspends in hardware (try_wait with a suspend-time hint) instead of
+// spinning, so it gives its issue slots to the warps that have work.
+constexpr unsigned kSuspendNs = 20000;
 __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
     asm volatile(
         "{\n .reg .pred P1;\n"
         "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(b)),
-        "r"(parity)
+        "r"(parity), "r"(kSuspendNs)
         : "memory");
 }
 
 template <int CPL, bool C64, bool BWD, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) {
+__global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepParams p) {
     using SW = Sweep<CPL, C64, BWD, NW>;
     constexpr int R = SW::R;
     constexpr int DP = SW::DP;
@@ -188,16 +197,23 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
     uint64_t *bars = reinterpret_cast<uint64_t *>(wsc + (BWD ? size_t(NW) * DP : 0));
     // full[w][s]: slot s of warp w's ring holds complete data (32 producer lanes arrive)
     // empty[w][s]: the consumer (warp w+1) is done with slot s (32 consumer lanes arrive)
+    // pub_full[k] / pub_empty[k]: band producer -> publisher warp handoff (kPubDepth deep)
+    uint64_t *pub_full = bars + 2 * NW * kRing;
+    uint64_t *pub_empty = pub_full + kPubDepth;
 
     // Zero the path-vector rings: a zero vector with m = 0 makes the recursion return
     // L = C, i.e. every slot nobody writes acts as a path start.
     {
         uint4 *z = reinterpret_cast<uint4 *>(smem_raw);
         const int n16 = int((size_t(NW) * kRing + kRing0) * VEC * 2 / 16);
-        for (int k = threadIdx.x; k < n16; k += NW * 32) z[k] = make_uint4(0u, 0u, 0u, 0u);
+        for (int k = threadIdx.x; k < n16; k += (NW + 1) * 32) z[k] = make_uint4(0u, 0u, 0u, 0u);
     }
     __shared__ int s_ticket;
     if (threadIdx.x < 2 * NW * kRing) mbar_init(bars + threadIdx.x, 32);
+    if (threadIdx.x < kPubDepth) {
+        mbar_init(pub_full + threadIdx.x, 32);
+        mbar_init(pub_empty + threadIdx.x, 1);
+    }
     if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
@@ -210,9 +226,30 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
     const int warp = int(__reduce_min_sync(0xffffffffu, threadIdx.x >> 5));
     const int lane = lane_id();
     const int W = p.W, H = p.H;
+    if (warp == NW) {
+        // Publisher warp: turns the band producer's completed position groups into the
+        // gpu-scope progress flag the next band polls.  The gpu-scope fence (a round trip
+        // to L2) runs here, off the producer's critical path.  Causality: producer lanes'
+        // gbuf stores -> mbarrier arrive (release.cta) -> wait here (acquire.cta) ->
+        // fence.acq_rel.gpu -> flag store (cumulative release).
+        if (band + 1 < p.nbands && !(p.debug_flags & 1)) {
+            int *prog = p.progress + view * p.nbands + band;
+            const int ngroups = (W + kPublish - 1) / kPublish;
+            for (int k = 0; k < ngroups; ++k) {
+                mbar_wait(pub_full + (k % kPubDepth), unsigned(k / kPubDepth) & 1u);
+                asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+                if (lane == 0) {
+                    st_relaxed_gpu(prog, min((k + 1) * kPublish, W));
+                    mbar_arrive(pub_empty + (k % kPubDepth));
+                }
+                __syncwarp();
+            }
+        }
+        return;
+    }
     const int j = band * NW + warp;                 // iteration row
     if (j >= H) return;                             // rows past the image (last band)
-    const bool has_row_below = (warp < NW - 1) && (j + 1 < H);
+    const bool has_row_below = (warp < NW - 1) && (j + 1 < H) && !(p.debug_flags & 1);
     const int y = BWD ? (H - 1 - j) : j;
 
     const uint64_t *ref, *match;
@@ -274,13 +311,13 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
     // band handoff (gbuf row has the same consumer-centric layout per position)
     const int nb_id = view * p.nbands + band;
     const bool has_consumer = band + 1 < p.nbands;
-    const bool is_producer = (warp == NW - 1) && has_consumer;
+    const bool is_producer = (warp == NW - 1) && has_consumer && !(p.debug_flags & 1);
     uint16_t *gout = p.gbuf + (long long)nb_id * W * VEC + dbase;
     const uint16_t *gin = p.gbuf + (long long)(nb_id - 1) * W * VEC;
-    int *prog_out = p.progress + nb_id;
     const int *prog_in = p.progress + (nb_id - 1);
-    const bool band_input = (warp == 0) && band > 0;
-    const bool ring_input = warp > 0;
+    const bool nodeps = (p.debug_flags & 1) != 0;
+    const bool band_input = (warp == 0) && band > 0 && !nodeps;
+    const bool ring_input = warp > 0 && !nodeps;
     int known = 0;                                  // producer progress seen (warp 0)
     constexpr int kChunks = VEC * 2 / 16;           // 16-byte chunks per position
 
@@ -290,7 +327,8 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
             if (known < need) {
                 int k, spins = 0;
                 // bounded wait: a logic error must not hang the GPU (~>2 s of polling)
-                while ((k = ld_acquire_gpu(prog_in)) < need && ++spins < (1 << 25)) __nanosleep(64);
+                while ((k = ld_relaxed_gpu(prog_in)) < need && ++spins < (1 << 25)) __nanosleep(32);
+                asm volatile("fence.acq_rel.gpu;\n" ::: "memory");   // acquire what k covers
                 known = k;
             }
             const char *g = reinterpret_cast<const char *>(gin + (long long)q * VEC);
@@ -349,6 +387,15 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
     float *dsub_row = do_wta ? p.dsub + (long long)view * p.disp_view_stride + yrow : nullptr;
     const int Dm1 = p.D - 1;
     __syncwarp();
+    unsigned long long *trace = p.trace ? p.trace + (size_t(ticket) * (NW + 1) + warp) * 4 : nullptr;
+    if (trace && lane == 0) {
+        unsigned long long t;
+        unsigned sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        trace[0] = t;
+        trace[2] = sm;
+    }
 
 #pragma unroll 1
     for (int i0 = 0; i0 < W; i0 += CPL) {
@@ -357,11 +404,6 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
             const int i = i0 + ph;
             if (i >= W) break;
             const int xv = xview(i);
-            // --- band output publication (producer warp, before this step's stores)
-            if (is_producer && i > 0 && ((i % kPublish) == 0)) {
-                __threadfence();
-                if (lane == 0) st_relaxed_gpu(prog_out, i);
-            }
             // --- inputs of the row above
             if (band_input) {
                 issue_input(i + kLook);
@@ -464,6 +506,12 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
                 if (i > 0) VecIO<R>::st(g - VEC + 2 * DP, nv[2]);
                 if (i == 0) VecIO<R>::st(g + DP, zero);            // no (i-1) predecessor
                 if (i == W - 1) VecIO<R>::st(g + 2 * DP, zero);    // no (i+1) predecessor
+                if ((i + 1) % kPublish == 0 || i == W - 1) {       // hand group k to the publisher
+                    const int k = i / kPublish;
+                    if (k >= kPubDepth)
+                        mbar_wait(pub_empty + (k % kPubDepth), unsigned(k / kPubDepth - 1) & 1u);
+                    mbar_arrive(pub_full + (k % kPubDepth));
+                }
             }
             // --- sweep output
             if (!BWD) {
@@ -540,23 +588,25 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_kernel(const SweepParams p) 
         VecIO<R>::st(my_ring + size_t((W - 1) & (kRing - 1)) * VEC + 2 * DP, zero);
         mbar_arrive(my_full + ((W - 1) & (kRing - 1)));
     }
-    if (is_producer) {
-        __threadfence();
-        if (lane == 0) st_relaxed_gpu(prog_out, W);
-    }
     if (band_input) cp_async_wait<0>();
+    if (trace && lane == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        trace[1] = t;
+    }
 }
 
 template <int CPL, bool C64, int NW>
 cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cudaEvent_t ev_mid_a,
                         cudaEvent_t ev_mid_b, int *launches, int *sync_buf, size_t sync_bytes) {
     (void)debug_s;
-    const dim3 grid(p.nviews * p.nbands), block(NW * 32);
+    const dim3 grid(p.nviews * p.nbands), block((NW + 1) * 32);
     cudaError_t e;
     {
         constexpr size_t sm = Sweep<CPL, C64, false, NW>::smem_bytes();
         auto k = sweep_kernel<CPL, C64, false, NW>;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(sync_buf, 0, sync_bytes, st)) != cudaSuccess) return e;
         k<<<grid, block, sm, st>>>(p);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -568,6 +618,7 @@ cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cud
         constexpr size_t sm = Sweep<CPL, C64, true, NW>::smem_bytes();
         auto k = sweep_kernel<CPL, C64, true, NW>;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(sync_buf, 0, sync_bytes, st)) != cudaSuccess) return e;
         k<<<grid, block, sm, st>>>(p);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
