@@ -53,7 +53,8 @@ typedef struct sgm_params {
     int32_t height;         /* H >= 1 */
     int32_t num_disp;       /* D disparity levels, d in [0, D-1] (G6); 1 <= D <= 256 */
     int32_t census_w;       /* census window width, odd (G2) */
-    int32_t census_h;       /* census window height, odd; census_w*census_h-1 <= 64 */
+    int32_t census_h;       /* census window height, odd; census_w*census_h-1 <= 63 (the
+                               backward sweep reads the cost from 6 spare bits of S_fwd) */
     int32_t p1;             /* small-jump penalty P1, 0 <= P1 <= P2 (G8) */
     int32_t p2;             /* large-jump penalty P2; C_max + P2 <= 255 where
                                C_max = census_w*census_h-1 (G5, G9) */
@@ -90,7 +91,7 @@ typedef struct sgm_sceneflow_out {
 
 /* Create a handle on `device` (cudaSetDevice is called): validates `p`
  * (SGM_ERR_INVALID_ARGUMENT on: W or H < 1, D outside 1..256, even census
- * side, census_w*census_h-1 > 64, P1 < 0, P2 < P1, C_max+P2 > 255, T < 0,
+ * side, census_w*census_h-1 > 63, P1 < 0, P2 < P1, C_max+P2 > 255, T < 0,
  * bilinear_rule not 0/1, max_batch < 1) and allocates all scratch for
  * max_batch quads (SGM_ERR_OUT_OF_MEMORY if that fails).  Synchronous.
  * `*out` is set only on SGM_OK. */

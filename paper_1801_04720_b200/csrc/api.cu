@@ -92,6 +92,7 @@ sgm::SweepParams sweep_params(const sgm_handle *h, int nviews) {
         return e ? atoi(e) : 0;
     }();
     p.debug_flags = dbg;
+    p.one = 1;
     return p;
 }
 
@@ -125,7 +126,7 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     const int W = p->width, H = p->height, D = p->num_disp;
     const int cw = p->census_w, ch = p->census_h;
     if (W < 1 || H < 1 || D < 1 || D > 256) return SGM_ERR_INVALID_ARGUMENT;
-    if (cw < 1 || ch < 1 || (cw % 2) == 0 || (ch % 2) == 0 || cw * ch - 1 > 64 || cw * ch < 2)
+    if (cw < 1 || ch < 1 || (cw % 2) == 0 || (ch % 2) == 0 || cw * ch - 1 > 63 || cw * ch < 2)
         return SGM_ERR_INVALID_ARGUMENT;
     if (cw > 17 || ch > 17) return SGM_ERR_UNSUPPORTED;      // TMA box halo limits
     if (p->p1 < 0 || p->p2 < p->p1 || (cw * ch - 1) + p->p2 > 255) return SGM_ERR_INVALID_ARGUMENT;

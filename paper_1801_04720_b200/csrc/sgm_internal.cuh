@@ -45,6 +45,7 @@ struct SweepParams {
     int *ticket;              // CTA ticket counter (zeroed before launch)
     unsigned long long *trace; // debug: per (ticket, warp) {start ns, end ns, smid, 0} or null
     int debug_flags;           // debug (env SGM_DEBUG_FLAGS): 1 = no inter-warp/band waits
+    int one;                   // always 1 (opaque to the compiler: keeps adds on the FMA pipe)
 };
 
 struct CensusParams {

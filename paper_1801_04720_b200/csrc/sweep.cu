@@ -95,11 +95,6 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 __device__ __forceinline__ int ld_relaxed_gpu(const int *p) {
     int v;
     asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -109,20 +104,31 @@ __device__ __forceinline__ void st_relaxed_gpu(int *p, int v) {
     asm volatile("st.relaxed.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
+// Integer multiply-add on the FMA pipe.  `one` is a runtime 1 (kernel parameter), so
+// ptxas cannot fold a*one+c into an ALU-pipe IADD3: the min-plus work saturates the
+// half-rate ALU pipe (VIMNMX / VIADDMNMX / PRMT / LOP3 all issue there), while IMAD
+// issues on the otherwise idle FMA pipe.
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 // One semi-global path update for the CPL cells a lane holds.
 //   prev: L_r(p - r, .) (u16x2 pairs), C: C(p, .), out: L_r(p, .).
 //   sel_up / sel_dn: PRMT selectors building the d-1 / d+1 neighbour pairs (per lane).
 template <int R>
 __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uint32_t (&C)[R],
                                             uint32_t (&out)[R], uint32_t p1x2, uint32_t p2x2,
-                                            uint32_t sel_up, uint32_t sel_dn) {
-    // m = min_k L_r(p - r, k), broadcast as m * 0x10001
+                                            uint32_t sel_up, uint32_t sel_dn, uint32_t one) {
+    // m = min_k L_r(p - r, k): min over the lane's pairs, then over the two halves (the
+    // high half is brought down with IMAD.HI on the FMA pipe), then over the warp
     uint32_t v = prev[0];
 #pragma unroll
     for (int r = 1; r < R; ++r) v = __vminu2(v, prev[r]);
-    v = __vminu2(v, __byte_perm(v, 0, 0x1032));
-    const uint32_t mm = __reduce_min_sync(0xffffffffu, v);
-    const uint32_t mP2 = mm + p2x2;      // m + P2 in both halves
+    v = __vminu2(v, __umulhi(v, 0x10000u));           // lo = min(lo, hi), hi = 0
+    const uint32_t m = __reduce_min_sync(0xffffffffu, v);
+    const uint32_t mP2 = imad(m, 0x10001u, p2x2);     // m + P2 in both halves
     // neighbours d-1 / d+1
     const uint32_t up = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
     const uint32_t dn = __shfl_down_sync(0xffffffffu, prev[0], 1);
@@ -136,7 +142,8 @@ __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uin
         uint32_t t = __vminu2(nb[r], nb[r + 1]);       // min(L(d-1), L(d+1))
         t = __viaddmin_u16x2(t, p1x2, prev[r]);        // min(.. + P1, L(d))
         t = __vminu2(t, mP2);                          // min(.., m + P2)
-        out[r] = t + C[r] - mm;                        // + C - m (carry-exact)
+        // + C - m in both halves: exact mod 2^32 since each half's result is in [0, 2^16)
+        out[r] = t + C[r] - m * 0x10001u;
     }
 }
 
@@ -275,9 +282,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     uint16_t *sfwd_ptr = sfwd_row + (BWD ? (long long)(W - 1) * DP : 0);
 
     // per-lane constants
+    const uint32_t one = uint32_t(p.one);
     const uint32_t p1x2 = uint32_t(p.P1) * 0x10001u;
     const uint32_t p2x2 = uint32_t(p.P2) * 0x10001u;
     const int dbase = CPL * lane;
+    const bool has_pad = p.D < DP;
     // PRMT selectors for the d-1 / d+1 neighbour pairs: at d = 0 (lane 0) the missing d-1
     // candidate is replaced by the d+1 one (min(L(1), L(1)) == min over existing terms,
     // G7) and symmetrically at d = Dp-1 (lane 31).
@@ -339,8 +348,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
         cp_async_commit();
     };
 
-    // census prefetch: positions 0..63
-    for (int k = lane; k < 64; k += 32) {
+    // census prefetch: positions 0..63 (forward sweep only: the backward sweep reads the
+    // matching cost the forward sweep packed into S_fwd)
+    for (int k = lane; k < 64 && !BWD; k += 32) {
         if (k < W) {
             const int xv = xview(k);
             int xm = xv - (BWD ? DP - 1 : 0);
@@ -364,15 +374,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     CW win[CPL];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) win[k] = 0;
-    if (BWD) {
-        // logical window before the first rotation: cm(W - d) (see the slide below)
-#pragma unroll
-        for (int jj = 0; jj < CPL; ++jj) {
-            int xm = W - (dbase + jj);
-            xm = xm < 0 ? 0 : (xm > W - 1 ? W - 1 : xm);
-            win[(jj + CPL - 1) % CPL] = CW(__ldg(match_row + X(xm)));
-        }
-    }
     uint32_t pf[2][R];                               // BWD: S_fwd prefetch (2 positions)
 #pragma unroll
     for (int r = 0; r < R; ++r) { pf[0][r] = 0; pf[1][r] = 0; }
@@ -413,7 +414,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                 mbar_wait(src_full + (i & (kRing - 1)), unsigned(i / kRing) & 1u);
             }
             // --- census prefetch refill
-            if ((i & 31) == 0) {
+            if (BWD) {
+            } else if ((i & 31) == 0) {
                 const int q = i + 32 + lane;
                 if (q < W) {
                     const int xq = xview(q);
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                 __syncwarp();
             }
             // --- slide the census window by one position
-            {
+            if (!BWD) {
                 const uint64_t fresh = cfresh[i & 63];
                 if (!BWD) {
                     const int q = (CPL - ph) % CPL;       // outgoing logical CPL-1
@@ -443,16 +445,33 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                     win[q] = lane == 31 ? CW(fresh) : v;
                 }
             }
-            // --- matching cost C(x', d) for the lane's CPL cells
-            uint32_t C[R];
-            {
+            // --- matching cost C(x', d) for the lane's CPL cells.  The forward sweep
+            // computes it from the census window; the backward sweep unpacks it from the
+            // S_fwd word the forward sweep stored: word = S_fwd << 6 | C (S_fwd <= 4 *
+            // (C_max + P2) <= 1020 < 2^10, C <= C_max <= 63 < 2^6; sgm_create enforces both).
+            uint32_t C[R], craw[R], Sf[R];
+            if (BWD) {
+                const int slot = ph & 1;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    craw[r] = pf[slot][r] & 0x003F003Fu;
+                    Sf[r] = (pf[slot][r] >> 6) & 0x03FF03FFu;
+                    C[r] = craw[r] + pad[r];
+                }
+                if (i + 2 < W) VecIO<R>::ld(sfwd_ptr + 2 * sstep, pf[slot]);
+                sfwd_ptr += sstep;
+            } else {
                 const uint64_t rv = cref[i & 63];
                 uint32_t c[CPL];
 #pragma unroll
                 for (int jj = 0; jj < CPL; ++jj) {
                     const int phys = BWD ? (jj + ph) % CPL : (jj - ph + CPL) % CPL;
-                    if (C64) c[jj] = __popcll(rv ^ uint64_t(win[phys]));
-                    else c[jj] = __popc(uint32_t(rv) ^ uint32_t(win[phys]));
+                    if (C64) {
+                        const uint64_t x = rv ^ uint64_t(win[phys]);
+                        c[jj] = imad(uint32_t(__popc(uint32_t(x))), one, uint32_t(__popc(uint32_t(x >> 32))));
+                    } else {
+                        c[jj] = __popc(uint32_t(rv) ^ uint32_t(win[phys]));
+                    }
                 }
                 if (xv < Dm1) {                            // border: x' - d < 0 -> C_max
 #pragma unroll
@@ -460,7 +479,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                         if (dbase + jj > xv) c[jj] = uint32_t(p.cmax);
                 }
 #pragma unroll
-                for (int r = 0; r < R; ++r) C[r] = __byte_perm(c[2 * r], c[2 * r + 1], 0x5410) | pad[r];
+                for (int r = 0; r < R; ++r) {
+                    craw[r] = imad(c[2 * r + 1], 0x10000u, c[2 * r]);
+                    C[r] = craw[r] + pad[r];
+                }
             }
             // --- row-above predecessors: all three live in slot i
             uint32_t pv[3][R];
@@ -477,14 +499,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             uint32_t S[R];
             {
                 uint32_t nL[R];
-                path_update<R>(Lh, C, nL, p1x2, p2x2, sel_up, sel_dn);
+                path_update<R>(Lh, C, nL, p1x2, p2x2, sel_up, sel_dn, one);
 #pragma unroll
                 for (int r = 0; r < R; ++r) { Lh[r] = nL[r]; S[r] = nL[r]; }
             }
             uint32_t nv[3][R];
 #pragma unroll
             for (int v = 0; v < 3; ++v) {
-                path_update<R>(pv[v], C, nv[v], p1x2, p2x2, sel_up, sel_dn);
+                path_update<R>(pv[v], C, nv[v], p1x2, p2x2, sel_up, sel_dn, one);
 #pragma unroll
                 for (int r = 0; r < R; ++r) S[r] += nv[v][r];
             }
@@ -515,15 +537,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             }
             // --- sweep output
             if (!BWD) {
-                VecIO<R>::st(sfwd_ptr, S);
+                uint32_t w[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    // padded disparities (d >= D) carry huge sums: saturate them to 10 bits,
+                    // the backward sweep re-applies the padding cost anyway
+                    const uint32_t sv = has_pad ? __vminu2(S[r], 0x03FF03FFu) : S[r];
+                    w[r] = imad(sv, 64u, craw[r]);
+                }
+                VecIO<R>::st(sfwd_ptr, w);
                 sfwd_ptr += sstep;
             } else {
                 uint32_t St[R];
-                const int slot = ph & 1;
 #pragma unroll
-                for (int r = 0; r < R; ++r) St[r] = S[r] + pf[slot][r];
-                if (i + 2 < W) VecIO<R>::ld(sfwd_ptr + 2 * sstep, pf[slot]);
-                sfwd_ptr += sstep;
+                for (int r = 0; r < R; ++r) St[r] = S[r] + Sf[r];
                 if (do_sout) {
                     const int x = X(xv);
 #pragma unroll
