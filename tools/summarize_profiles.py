@@ -1,0 +1,117 @@
+#!/usr/bin/env python
+"""Turn the round's gpurun_out/ artefacts into tracked summaries under profiles/:
+  profiles/<tag>_launches.md    per-kernel share of a bench step (ncu launch list)
+  profiles/<tag>_sweep_ncu.md   ncu --set full summary of the sweep kernels
+  profiles/ncu_traffic.json     dram bytes per launch of the sweep kernels (bench.py reads it)
+  profiles/<tag>_bench.json     the bench JSON line
+Usage: python tools/summarize_profiles.py <tag>"""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+
+def short(name):
+    for k in ("sweep_kernel<", "census_kernel", "lr_kernel", "combine_kernel", "cost_kernel", "wta_kernel"):
+        if k in name:
+            if k == "sweep_kernel<":
+                args = name.split("sweep_kernel<")[1].split(">")[0]
+                return "sweep_bwd_wta" if args.split(",")[2].strip() in ("1", "true", "(bool)1") else "sweep_fwd"
+            return k
+    return name[:40]
+
+
+def launches(tag):
+    rows = list(csv.reader(open(os.path.join(OUT, "launches.csv"))))
+    hdr = None
+    data = []
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d.get("Metric Name") == "gpu__time_duration.sum":
+                data.append(d)
+    tot = collections.defaultdict(float)
+    cnt = collections.Counter()
+    for d in data:
+        k = short(d["Kernel Name"])
+        v = float(d["Metric Value"].replace(",", ""))
+        unit = d["Metric Unit"]
+        v = v / 1e3 if unit == "nsecond" else (v if unit == "usecond" else v * 1e3)
+        tot[k] += v
+        cnt[k] += 1
+    s = sum(tot.values())
+    lines = [f"# {tag}: kernel launch list (ncu gpu__time_duration, --clock-control none)", "",
+             "Command: `python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-graph` "
+             "(8 Driving quads per step; ncu serialises launches and runs cold, so compare shares).", "",
+             "| kernel | launches | total us | us/launch | share |", "|---|---|---|---|---|"]
+    for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+        lines.append(f"| {k} | {cnt[k]} | {v:.1f} | {v / cnt[k]:.1f} | {100 * v / s:.1f}% |")
+    open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+def ncu_rows(rep, *args):
+    out = subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+    return list(csv.reader(io.StringIO(out)))
+
+
+def full(tag):
+    rep = os.path.join(OUT, "prof_sweep_round.ncu-rep")
+    rows = ncu_rows(rep, "--page", "raw", "--csv")
+    hdr, units = rows[0], rows[1]
+    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
+            "sm__inst_executed.avg.per_cycle_active",
+            "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+            "launch__grid_size", "launch__block_size", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+    lines = [f"# {tag}: ncu --set full of the sweep kernels", "",
+             "Command: `ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -c 2 "
+             "python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-graph` (launches of 32 "
+             "Driving views = 8 quads).", ""]
+    traffic = {}
+    for row in rows[2:]:
+        d = dict(zip(hdr, row))
+        name = short(d["Kernel Name"])
+        lines += [f"## {name} (`{d['Kernel Name'][:90]}`)", "", "| metric | value | unit |", "|---|---|---|"]
+        for k in keys:
+            if k in d:
+                lines.append(f"| {k} | {d[k]} | {units[hdr.index(k)]} |")
+        st = [(k, float(v)) for k, v in d.items() if k.startswith("smsp__average_warps_issue_stalled_")
+              and k.endswith("_per_issue_active.ratio") and v not in ("", "n/a")]
+        st.sort(key=lambda kv: -kv[1])
+        lines += ["", "Top stall reasons (warp cycles per issued instruction): " +
+                  ", ".join(f"{k[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]}={v:.2f}"
+                            for k, v in st[:8]), ""]
+        def gb(k):
+            v = float(d[k].replace(",", ""))
+            u = units[hdr.index(k)]
+            return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        traffic[name] = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
+    open(os.path.join(PROF, f"{tag}_sweep_ncu.md"), "w").write("\n".join(lines) + "\n")
+    json.dump({k: v for k, v in traffic.items()}, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    tag = sys.argv[1]
+    os.makedirs(PROF, exist_ok=True)
+    launches(tag)
+    full(tag)
+    b = os.path.join(OUT, "bench_full.json")
+    if os.path.exists(b):
+        open(os.path.join(PROF, f"{tag}_bench.json"), "w").write(open(b).read())
