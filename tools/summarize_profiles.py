@@ -46,7 +46,9 @@ def launches(tag):
         k = short(d["Kernel Name"])
         v = float(d["Metric Value"].replace(",", ""))
         unit = d["Metric Unit"]
-        v = v / 1e3 if unit == "nsecond" else (v if unit == "usecond" else v * 1e3)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                 "second": 1e6, "s": 1e6}
+        v = v * scale.get(unit, 1.0)
         tot[k] += v
         cnt[k] += 1
     s = sum(tot.values())
