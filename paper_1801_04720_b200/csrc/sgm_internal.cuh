@@ -9,7 +9,8 @@ namespace sgm {
 
 // ----------------------------------------------------------------- constants
 constexpr int kWarp = 32;
-constexpr int kRing = 8;        // intra-CTA row->row handoff ring (positions, mbarrier per slot)
+constexpr int kRing = 8;        // row->row handoff ring (positions) for CPL > 4
+constexpr int kRingWide = 16;   // ... for CPL <= 4 (fits 16 warps x 16 x 3 x 256 B)
 constexpr int kRing0 = 16;      // band-input ring of warp 0 (positions)
 constexpr int kLook = 8;        // band-input prefetch distance (positions)
 constexpr int kPublish = 8;     // band-output progress publication granularity (positions)

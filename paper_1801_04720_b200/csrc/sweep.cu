@@ -152,16 +152,23 @@ struct Sweep {
     static constexpr int R = CPL / 2;
     static constexpr int DP = 32 * CPL;
     static constexpr int VEC = 3 * DP;             // u16 per ring slot (3 path vectors)
+    // Row->row handoff: a ring of RS position slots per warp, synchronised in groups of G
+    // consecutive positions (one full-wait / empty-release per group).  The consumer of
+    // group g needs the producer to have finished position (g+1)G, and the producer may
+    // run at most ~RS-G positions ahead; RS = 16 needs 16 x 3 x Dp x 2 bytes per warp.
+    static constexpr int RS = (CPL <= 4) ? kRingWide : kRing;
+    static constexpr int G = (CPL <= 4) ? CPL : 1;   // groups align with the unrolled block
+    static constexpr int RG = RS / G;              // groups per ring
 
     static constexpr size_t smem_bytes() {
         size_t b = 0;
-        b += size_t(NW) * kRing * VEC * 2;          // ring
+        b += size_t(NW) * RS * VEC * 2;             // ring
         b += size_t(kRing0) * VEC * 2;              // band input ring
         b += size_t(NW) * 2 * 64 * 8;               // census prefetch (ref, fresh)
         if (BWD) {
             b += size_t(NW) * DP * 2;               // WTA scratch
         }
-        b += size_t(2) * NW * kRing * 8;            // full / empty mbarriers
+        b += size_t(2) * NW * RG * 8;               // full / empty mbarriers
         b += size_t(2) * kPubDepth * 8;             // publisher mbarriers
         return b;
     }
@@ -195,28 +202,31 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     constexpr int R = SW::R;
     constexpr int DP = SW::DP;
     constexpr int VEC = SW::VEC;
+    constexpr int RS = SW::RS;
+    constexpr int G = SW::G;
+    constexpr int RG = SW::RG;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint16_t *ring = reinterpret_cast<uint16_t *>(smem_raw);
-    uint16_t *in0 = ring + size_t(NW) * kRing * VEC;
+    uint16_t *in0 = ring + size_t(NW) * RS * VEC;
     uint64_t *cbuf = reinterpret_cast<uint64_t *>(in0 + size_t(kRing0) * VEC);
     uint16_t *wsc = reinterpret_cast<uint16_t *>(cbuf + size_t(NW) * 2 * 64);
     uint64_t *bars = reinterpret_cast<uint64_t *>(wsc + (BWD ? size_t(NW) * DP : 0));
     // full[w][s]: slot s of warp w's ring holds complete data (32 producer lanes arrive)
     // empty[w][s]: the consumer (warp w+1) is done with slot s (32 consumer lanes arrive)
     // pub_full[k] / pub_empty[k]: band producer -> publisher warp handoff (kPubDepth deep)
-    uint64_t *pub_full = bars + 2 * NW * kRing;
+    uint64_t *pub_full = bars + 2 * NW * RG;
     uint64_t *pub_empty = pub_full + kPubDepth;
 
     // Zero the path-vector rings: a zero vector with m = 0 makes the recursion return
     // L = C, i.e. every slot nobody writes acts as a path start.
     {
         uint4 *z = reinterpret_cast<uint4 *>(smem_raw);
-        const int n16 = int((size_t(NW) * kRing + kRing0) * VEC * 2 / 16);
+        const int n16 = int((size_t(NW) * RS + kRing0) * VEC * 2 / 16);
         for (int k = threadIdx.x; k < n16; k += (NW + 1) * 32) z[k] = make_uint4(0u, 0u, 0u, 0u);
     }
     __shared__ int s_ticket;
-    if (threadIdx.x < 2 * NW * kRing) mbar_init(bars + threadIdx.x, 32);
+    if (threadIdx.x < 2 * NW * RG) mbar_init(bars + threadIdx.x, 32);
     if (threadIdx.x < kPubDepth) {
         mbar_init(pub_full + threadIdx.x, 32);
         mbar_init(pub_empty + threadIdx.x, 1);
@@ -307,12 +317,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     //   v2 = L_anti(q+1) (predecessor of the (-1,1) path).
     // The producer at position p writes v0 -> slot p, v1 -> slot p+1, v2 -> slot p-1, and
     // arrives on full[p-1] (its v2 is the last write into that slot).
-    uint16_t *my_ring = ring + size_t(warp) * kRing * VEC + dbase;
-    const uint16_t *src_ring = (warp == 0 ? in0 : ring + size_t(warp - 1) * kRing * VEC) + dbase;
-    uint64_t *my_full = bars + size_t(warp) * kRing;
-    uint64_t *my_empty = bars + size_t(NW + warp) * kRing;           // released by warp+1
-    uint64_t *src_full = bars + size_t(warp - 1) * kRing;            // (warp >= 1)
-    uint64_t *src_empty = bars + size_t(NW + warp - 1) * kRing;
+    uint16_t *my_ring = ring + size_t(warp) * RS * VEC + dbase;
+    const uint16_t *src_ring = (warp == 0 ? in0 : ring + size_t(warp - 1) * RS * VEC) + dbase;
+    uint64_t *my_full = bars + size_t(warp) * RG;
+    uint64_t *my_empty = bars + size_t(NW + warp) * RG;              // released by warp+1
+    uint64_t *src_full = bars + size_t(warp - 1) * RG;               // (warp >= 1)
+    uint64_t *src_empty = bars + size_t(NW + warp - 1) * RG;
     uint64_t *cref = cbuf + size_t(warp) * 128;
     uint64_t *cfresh = cref + 64;
     uint16_t *wta = wsc + size_t(warp) * DP;
@@ -410,8 +420,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                 issue_input(i + kLook);
                 cp_async_wait<kLook>();
                 __syncwarp();
-            } else if (ring_input) {
-                mbar_wait(src_full + (i & (kRing - 1)), unsigned(i / kRing) & 1u);
+            } else if (ring_input && (ph % G) == 0) {
+                const int g = i / G;                       // group start: wait for slots
+                mbar_wait(src_full + (g % RG), unsigned(g / RG) & 1u);
             }
             // --- census prefetch refill
             if (BWD) {
@@ -487,13 +498,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             // --- row-above predecessors: all three live in slot i
             uint32_t pv[3][R];
             {
-                const uint16_t *src = src_ring + size_t(i & (band_input || warp == 0 ? kRing0 - 1 : kRing - 1)) * VEC;
+                const uint16_t *src = src_ring + size_t(i & (band_input || warp == 0 ? kRing0 - 1 : RS - 1)) * VEC;
 #pragma unroll
                 for (int v = 0; v < 3; ++v) VecIO<R>::ld(src + v * DP, pv[v]);
             }
-            if (ring_input) {
+            if (ring_input && (ph % G) == G - 1) {       // group end: release its slots
                 __syncwarp();
-                mbar_arrive(src_empty + (i & (kRing - 1)));
+                mbar_arrive(src_empty + ((i / G) % RG));
             }
             // --- the four path updates (->, down, two diagonals)
             uint32_t S[R];
@@ -512,12 +523,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             }
             // --- hand the three vectors to the row below
             if (has_row_below) {
-                if (i + 1 - kRing >= 0)                   // slot i+1 free again?
-                    mbar_wait(my_empty + ((i + 1) & (kRing - 1)), unsigned((i + 1) / kRing - 1) & 1u);
-                VecIO<R>::st(my_ring + size_t(i & (kRing - 1)) * VEC, nv[0]);
-                VecIO<R>::st(my_ring + size_t((i + 1) & (kRing - 1)) * VEC + DP, nv[1]);
-                VecIO<R>::st(my_ring + size_t((i - 1) & (kRing - 1)) * VEC + 2 * DP, nv[2]);
-                if (i > 0) mbar_arrive(my_full + ((i - 1) & (kRing - 1)));
+                if ((ph % G) == G - 1) {                   // next group's slots free again?
+                    const int h = i / G + 1;
+                    if (h >= RG) mbar_wait(my_empty + (h % RG), unsigned(h / RG - 1) & 1u);
+                }
+                VecIO<R>::st(my_ring + size_t(i & (RS - 1)) * VEC, nv[0]);
+                VecIO<R>::st(my_ring + size_t((i + 1) & (RS - 1)) * VEC + DP, nv[1]);
+                VecIO<R>::st(my_ring + size_t((i - 1) & (RS - 1)) * VEC + 2 * DP, nv[2]);
+                if ((ph % G) == 0 && i > 0) mbar_arrive(my_full + ((i / G - 1) % RG));   // group done
             } else if (is_producer) {
                 uint16_t *g = gout + (long long)i * VEC;
                 uint32_t zero[R];
@@ -609,11 +622,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
         uint32_t zero[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) zero[r] = 0;
-        const int i = W;
-        if (i + 1 - kRing >= 0)
-            mbar_wait(my_empty + ((i + 1) & (kRing - 1)), unsigned((i + 1) / kRing - 1) & 1u);
-        VecIO<R>::st(my_ring + size_t((W - 1) & (kRing - 1)) * VEC + 2 * DP, zero);
-        mbar_arrive(my_full + ((W - 1) & (kRing - 1)));
+        VecIO<R>::st(my_ring + size_t((W - 1) & (RS - 1)) * VEC + 2 * DP, zero);
+        mbar_arrive(my_full + (((W - 1) / G) % RG));
     }
     if (band_input) cp_async_wait<0>();
     if (trace && lane == 0) {
