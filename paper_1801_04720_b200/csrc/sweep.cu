@@ -249,7 +249,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
         // to L2) runs here, off the producer's critical path.  Causality: producer lanes'
         // gbuf stores -> mbarrier arrive (release.cta) -> wait here (acquire.cta) ->
         // fence.acq_rel.gpu -> flag store (cumulative release).
-        if (band + 1 < p.nbands && !(p.debug_flags & 1)) {
+        if (band + 1 < p.nbands && !(p.debug_flags & 3)) {
             int *prog = p.progress + view * p.nbands + band;
             const int ngroups = (W + kPublish - 1) / kPublish;
             for (int k = 0; k < ngroups; ++k) {
@@ -330,19 +330,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     // band handoff (gbuf row has the same consumer-centric layout per position)
     const int nb_id = view * p.nbands + band;
     const bool has_consumer = band + 1 < p.nbands;
-    const bool is_producer = (warp == NW - 1) && has_consumer && !(p.debug_flags & 1);
+    const bool is_producer = (warp == NW - 1) && has_consumer && !(p.debug_flags & 3);
     uint16_t *gout = p.gbuf + (long long)nb_id * W * VEC + dbase;
     const uint16_t *gin = p.gbuf + (long long)(nb_id - 1) * W * VEC;
     const int *prog_in = p.progress + (nb_id - 1);
     const bool nodeps = (p.debug_flags & 1) != 0;
-    const bool band_input = (warp == 0) && band > 0 && !nodeps;
+    const bool noband = (p.debug_flags & 2) != 0;   // debug: no inter-band handoff
+    const bool band_input = (warp == 0) && band > 0 && !nodeps && !noband;
     const bool ring_input = warp > 0 && !nodeps;
     int known = 0;                                  // producer progress seen (warp 0)
     constexpr int kChunks = VEC * 2 / 16;           // 16-byte chunks per position
 
-    auto issue_input = [&](int q) {                 // cp.async gbuf[q] -> in0 slot q
-        if (q < W) {
-            const int need = min(q + 2, W);
+    // cp.async the band input of positions [hG, hG+G) (gbuf -> in0), one commit group
+    constexpr int LG = (kRing0 / G - 1) > 2 ? 2 : (kRing0 / G - 1);   // prefetch distance (groups)
+    auto issue_input = [&](int h) {
+        const int q0 = h * G;
+        if (q0 < W) {
+            const int need = min(q0 + G + 1, W);    // gbuf[q] is complete once q+1 is done
             if (known < need) {
                 int k, spins = 0;
                 // bounded wait: a logic error must not hang the GPU (~>2 s of polling)
@@ -350,10 +354,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                 asm volatile("fence.acq_rel.gpu;\n" ::: "memory");   // acquire what k covers
                 known = k;
             }
-            const char *g = reinterpret_cast<const char *>(gin + (long long)q * VEC);
-            char *s = reinterpret_cast<char *>(in0 + size_t(q & (kRing0 - 1)) * VEC);
+            const char *g = reinterpret_cast<const char *>(gin + (long long)q0 * VEC) + 16 * lane;
+#pragma unroll 1
+            for (int q = q0; q < q0 + G && q < W; ++q, g += 2 * VEC) {
+                char *sm = reinterpret_cast<char *>(in0 + size_t(q & (kRing0 - 1)) * VEC) + 16 * lane;
 #pragma unroll
-            for (int c = lane; c < kChunks; c += 32) cp_async16(s + 16 * c, g + 16 * c);
+                for (int c = 0; c < kChunks; c += 32)
+                    if (c + lane < kChunks) cp_async16(sm + 16 * c, g + 16 * c);
+            }
         }
         cp_async_commit();
     };
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
 
     if (band_input) {
 #pragma unroll 1
-        for (int q = 0; q < kLook; ++q) issue_input(q);
+        for (int h = 0; h < LG; ++h) issue_input(h);
     }
 
     // state
@@ -417,9 +425,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             const int xv = xview(i);
             // --- inputs of the row above
             if (band_input) {
-                issue_input(i + kLook);
-                cp_async_wait<kLook>();
-                __syncwarp();
+                if ((ph % G) == 0) {                   // group start: keep LG groups in flight
+                    issue_input(i / G + LG);
+                    cp_async_wait<LG>();
+                    __syncwarp();
+                }
             } else if (ring_input && (ph % G) == 0) {
                 const int g = i / G;                       // group start: wait for slots
                 mbar_wait(src_full + (g % RG), unsigned(g / RG) & 1u);
