@@ -33,6 +33,9 @@ struct sgm_handle {
     uint8_t *lr_valid = nullptr;
     uint16_t *gbuf = nullptr;       // [4*max_batch][nbands][W][3][Dp]
     int *sync = nullptr;            // [1 + 4*max_batch*nbands]
+    int *sync_aux[2] = {nullptr, nullptr};   // per internal stream (pipelined host entry)
+    cudaStream_t aux[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_aux[2] = {nullptr, nullptr};
     // staging for the _host entry point (device)
     uint8_t *img_stage = nullptr;   // [max_batch][4][H][pitch]
     long long stage_pitch = 0;
@@ -68,24 +71,35 @@ cudaError_t dalloc(T **p, size_t count) {
 void free_all(sgm_handle *h) {
     void *ptrs[] = {h->census, h->sfwd, h->dint, h->dsub, h->lr_int, h->lr_sub, h->lr_valid,
                     h->gbuf, h->sync, h->img_stage, h->flow_stage, h->fvalid_stage,
-                    h->sf_stage, h->p0_stage, h->dp_stage, h->vsf_stage, h->v3_stage};
+                    h->sf_stage, h->p0_stage, h->dp_stage, h->vsf_stage, h->v3_stage,
+                    h->sync_aux[0], h->sync_aux[1]};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    for (auto &s : h->aux)
+        if (s) cudaStreamDestroy(s);
+    if (h->ev_start) cudaEventDestroy(h->ev_start);
+    for (auto &e : h->ev_aux)
+        if (e) cudaEventDestroy(e);
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
 }
 
-sgm::SweepParams sweep_params(const sgm_handle *h, int nviews) {
+// Sweep parameters for `nviews` views starting at quad `qoff` of the handle's scratch,
+// synchronising through `sync` (ticket + per-band progress flags).
+sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int qoff = 0, int *sync = nullptr) {
     sgm::SweepParams p{};
+    const long long v0 = 4LL * qoff;
     p.W = h->prm.width; p.H = h->prm.height; p.D = h->prm.num_disp; p.Dp = h->dp;
     p.P1 = h->prm.p1; p.P2 = h->prm.p2; p.cmax = h->cmax;
     p.nviews = nviews; p.nbands = h->nbands;
-    p.cen = h->census; p.cen_img_stride = h->npx;
+    p.cen = h->census + v0 * h->npx; p.cen_img_stride = h->npx;
     p.explicit_mode = 0;
-    p.sfwd = h->sfwd; p.sfwd_view_stride = h->npx * h->dp;
-    p.dint = h->dint; p.dsub = h->dsub; p.disp_view_stride = h->npx;
+    p.sfwd = h->sfwd + v0 * h->npx * h->dp; p.sfwd_view_stride = h->npx * h->dp;
+    p.dint = h->dint + v0 * h->npx; p.dsub = h->dsub + v0 * h->npx; p.disp_view_stride = h->npx;
     p.sout = nullptr;
-    p.gbuf = h->gbuf; p.progress = h->sync + 1; p.ticket = h->sync;
+    p.gbuf = h->gbuf + v0 * h->nbands * (long long)h->prm.width * 3 * h->dp;
+    if (!sync) sync = h->sync;
+    p.progress = sync + 1; p.ticket = sync;
     p.trace = h->trace;
     static const int dbg = [] {
         const char *e = getenv("SGM_DEBUG_FLAGS");
@@ -159,6 +173,10 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     if (e == cudaSuccess) e = dalloc(&h->lr_valid, nv / 2 * npx);
     if (e == cudaSuccess) e = dalloc(&h->gbuf, nv * size_t(h->nbands) * size_t(W) * 3 * size_t(h->dp));
     if (e == cudaSuccess) e = dalloc(&h->sync, 1 + nv * size_t(h->nbands));
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = dalloc(&h->sync_aux[k], 1 + nv * size_t(h->nbands));
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamCreateWithFlags(&h->aux[k], cudaStreamNonBlocking);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&h->ev_aux[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
     if (e == cudaSuccess) e = dalloc(&h->img_stage, nv * size_t(H) * size_t(h->stage_pitch));
     if (e == cudaSuccess) e = dalloc(&h->flow_stage, size_t(p->max_batch) * npx * 2);
     if (e == cudaSuccess) e = dalloc(&h->fvalid_stage, size_t(p->max_batch) * npx);
@@ -357,7 +375,7 @@ sgm_status sgm_combine_sceneflow(sgm_handle *h, const float *d0, const uint8_t *
 static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *images, int64_t pitch,
                                   const float *flow, const uint8_t *flow_valid,
                                   const sgm_camera *cam, const sgm_sceneflow_out *out,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, int qoff = 0, int *sync = nullptr) {
     const int W = h->prm.width, H = h->prm.height;
     const long long npx = h->npx;
     const bool want3d = out->p0 || out->dp || out->valid_3d;
@@ -369,12 +387,14 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *image
     };
     mark(0);
     cudaError_t e = sgm::launch_census_stack(images, (long long)H * pitch, 4 * n, pitch, W, H,
-                                             h->prm.census_w, h->prm.census_h, h->census, npx, st);
+                                             h->prm.census_w, h->prm.census_h,
+                                             h->census + 4LL * qoff * npx, npx, st);
     if (e != cudaSuccess) return from_cuda(e);
     ++h->launches;
     mark(1);
+    const long long v0 = 4LL * qoff * npx;
     {
-        sgm::SweepParams p = sweep_params(h, 4 * n);
+        sgm::SweepParams p = sweep_params(h, 4 * n, qoff, sync);
         int nl = 0;
         e = sgm::launch_sweeps(p, h->cpl, h->c64, h->nw, false, st, timing ? h->ev[2] : nullptr,
                                nullptr, &nl);
@@ -382,14 +402,14 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *image
         if (e != cudaSuccess) return from_cuda(e);
     }
     mark(3);
-    int16_t *di = out->disp_int ? out->disp_int : h->lr_int;
-    float *ds = out->disp_sub ? out->disp_sub : h->lr_sub;
-    uint8_t *dv = out->disp_valid ? out->disp_valid : h->lr_valid;
+    int16_t *di = out->disp_int ? out->disp_int : h->lr_int + 2LL * qoff * npx;
+    float *ds = out->disp_sub ? out->disp_sub : h->lr_sub + 2LL * qoff * npx;
+    uint8_t *dv = out->disp_valid ? out->disp_valid : h->lr_valid + 2LL * qoff * npx;
     {
         sgm::LrParams p{};
         p.W = W; p.H = H; p.T = h->prm.lr_threshold; p.invalid = h->prm.invalid_disp;
         p.npairs = 2 * n;
-        p.dl = h->dint; p.dls = h->dsub; p.dr = h->dint + npx;
+        p.dl = h->dint + v0; p.dls = h->dsub + v0; p.dr = h->dint + v0 + npx;
         p.in_stride_l = p.in_stride_r = 2 * npx;
         p.out_int = di; p.out_sub = ds; p.valid = dv; p.out_stride = npx;
         e = sgm::launch_lr(p, st);
@@ -435,40 +455,73 @@ sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, 
                                const sgm_sceneflow_out *out, void *stream) {
     if (!h || !images || !flow || !out || !out->sf || !out->valid_sf) return SGM_ERR_INVALID_ARGUMENT;
     if (n < 1 || n > h->prm.max_batch) return SGM_ERR_INVALID_ARGUMENT;
+    const bool want3d = out->p0 || out->dp || out->valid_3d;
+    if (want3d && (!out->p0 || !out->dp || !out->valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int W = h->prm.width, H = h->prm.height;
     const long long npx = h->npx;
-    cudaError_t e = cudaMemcpy2DAsync(h->img_stage, size_t(h->stage_pitch), images, size_t(W),
-                                      size_t(W), size_t(4LL * n * H), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(h->flow_stage, flow, sizeof(float) * 2 * npx * n, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && flow_valid)
-        e = cudaMemcpyAsync(h->fvalid_stage, flow_valid, size_t(npx) * n, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return from_cuda(e);
-    sgm_sceneflow_out dev{};
-    dev.sf = h->sf_stage;
-    dev.valid_sf = h->vsf_stage;
-    const bool want3d = out->p0 || out->dp || out->valid_3d;
-    if (want3d) { dev.p0 = h->p0_stage; dev.dp = h->dp_stage; dev.valid_3d = h->v3_stage; }
     const bool want_disp = out->disp_int || out->disp_sub || out->disp_valid;
-    sgm_status s = scene_flow_impl(h, n, h->img_stage, h->stage_pitch, h->flow_stage,
-                                   flow_valid ? h->fvalid_stage : nullptr, cam, &dev, st);
+    // Pipeline over chunks of quads on two internal streams: the host->device copy of
+    // chunk c+1 and the device->host copy of chunk c-1 overlap the kernels of chunk c
+    // (the copy engines run beside the SMs; each stream has its own sweep sync buffers).
+    const int chunk = n >= 4 ? 2 : n;
+    const bool timing = h->timing;
+    h->timing = false;
+    cudaError_t e = cudaEventRecord(h->ev_start, st);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(h->aux[k], h->ev_start, 0);
+    sgm_status s = SGM_OK;
+    int c = 0;
+    for (int q0 = 0; q0 < n && e == cudaSuccess && s == SGM_OK; q0 += chunk, ++c) {
+        const int cq = n - q0 < chunk ? n - q0 : chunk;
+        cudaStream_t cs = h->aux[c & 1];
+        uint8_t *img_dev = h->img_stage + 4LL * q0 * H * h->stage_pitch;
+        float *flow_dev = h->flow_stage + 2LL * q0 * npx;
+        uint8_t *fv_dev = h->fvalid_stage + (long long)q0 * npx;
+        e = cudaMemcpy2DAsync(img_dev, size_t(h->stage_pitch), images + 4LL * q0 * H * W, size_t(W),
+                              size_t(W), size_t(4LL * cq * H), cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(flow_dev, flow + 2LL * q0 * npx, sizeof(float) * 2 * npx * cq,
+                                cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess && flow_valid)
+            e = cudaMemcpyAsync(fv_dev, flow_valid + (long long)q0 * npx, size_t(npx) * cq,
+                                cudaMemcpyHostToDevice, cs);
+        if (e != cudaSuccess) break;
+        sgm_sceneflow_out dev{};
+        dev.sf = h->sf_stage + 4LL * q0 * npx;
+        dev.valid_sf = h->vsf_stage + (long long)q0 * npx;
+        if (want3d) {
+            dev.p0 = h->p0_stage + 4LL * q0 * npx;
+            dev.dp = h->dp_stage + 4LL * q0 * npx;
+            dev.valid_3d = h->v3_stage + (long long)q0 * npx;
+        }
+        s = scene_flow_impl(h, cq, img_dev, h->stage_pitch, flow_dev, flow_valid ? fv_dev : nullptr,
+                            cam, &dev, cs, q0, h->sync_aux[c & 1]);
+        if (s != SGM_OK) break;
+        auto d2h = [&](void *dst, const void *src, size_t bytes) {
+            if (dst && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs);
+        };
+        d2h(out->sf ? out->sf + 4LL * q0 * npx : nullptr, dev.sf, sizeof(float) * 4 * npx * cq);
+        d2h(out->valid_sf + (long long)q0 * npx, dev.valid_sf, size_t(npx) * cq);
+        if (want3d) {
+            d2h(out->p0 + 4LL * q0 * npx, dev.p0, sizeof(float) * 4 * npx * cq);
+            d2h(out->dp + 4LL * q0 * npx, dev.dp, sizeof(float) * 4 * npx * cq);
+            d2h(out->valid_3d + (long long)q0 * npx, dev.valid_3d, size_t(npx) * cq);
+        }
+        if (want_disp) {
+            const long long o = 2LL * q0 * npx;
+            d2h(out->disp_int ? out->disp_int + o : nullptr, h->lr_int + o, sizeof(int16_t) * 2 * npx * cq);
+            d2h(out->disp_sub ? out->disp_sub + o : nullptr, h->lr_sub + o, sizeof(float) * 2 * npx * cq);
+            d2h(out->disp_valid ? out->disp_valid + o : nullptr, h->lr_valid + o, size_t(2 * npx) * cq);
+        }
+    }
+    // the caller's stream waits for both internal streams
+    for (int k = 0; k < 2; ++k) {
+        cudaError_t e2 = cudaEventRecord(h->ev_aux[k], h->aux[k]);
+        if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, h->ev_aux[k], 0);
+        if (e == cudaSuccess) e = e2;
+    }
+    h->timing = timing;
     if (s != SGM_OK) return s;
-    auto d2h = [&](void *dst, const void *src, size_t bytes) {
-        if (dst && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
-    };
-    d2h(out->sf, h->sf_stage, sizeof(float) * 4 * npx * n);
-    d2h(out->valid_sf, h->vsf_stage, size_t(npx) * n);
-    if (want3d) {
-        d2h(out->p0, h->p0_stage, sizeof(float) * 4 * npx * n);
-        d2h(out->dp, h->dp_stage, sizeof(float) * 4 * npx * n);
-        d2h(out->valid_3d, h->v3_stage, size_t(npx) * n);
-    }
-    if (want_disp) {
-        d2h(out->disp_int, h->lr_int, sizeof(int16_t) * 2 * npx * n);
-        d2h(out->disp_sub, h->lr_sub, sizeof(float) * 2 * npx * n);
-        d2h(out->disp_valid, h->lr_valid, size_t(2 * npx) * n);
-    }
     return from_cuda(e);
 }
 

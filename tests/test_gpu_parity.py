@@ -261,8 +261,9 @@ def test_host_entry_point_matches_device(dev):
     from paper_1801_04720_b200 import SGM, Camera, stack_quads
     cfg = synth.CONFIGS["tiny"]
     prm = synth.sgm_params(cfg)
-    g = SGM.from_config(cfg, max_batch=2)
-    quads = [synth.make_quad(cfg, i) for i in range(2)]
+    n = 5                                   # chunked pipeline: chunks of 2, last one partial
+    g = SGM.from_config(cfg, max_batch=n)
+    quads = [synth.make_quad(cfg, i) for i in range(n)]
     imgs, flow = stack_quads(quads, g.pitch, dev)
     cam = Camera(prm["f"], prm["B"], prm["cx"], prm["cy"])
     ref = g.scene_flow(imgs, flow, cam)
@@ -270,7 +271,7 @@ def test_host_entry_point_matches_device(dev):
     himg = torch.from_numpy(np.stack([[q[k] for k in ("il0", "ir0", "il1", "ir1")]
                                       for q in quads])).pin_memory()
     hflow = torch.from_numpy(np.stack([q["flow"] for q in quads])).pin_memory()
-    hout = g.alloc_outputs(2, pinned_host=True)
+    hout = g.alloc_outputs(n, pinned_host=True)
     g.scene_flow_host(himg, hflow, cam, hout)
     torch.cuda.synchronize()
     for k in hout:
