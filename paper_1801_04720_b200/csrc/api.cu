@@ -33,9 +33,12 @@ struct sgm_handle {
     uint8_t *lr_valid = nullptr;
     uint16_t *gbuf = nullptr;       // [4*max_batch][nbands][W][3][Dp]
     int *sync = nullptr;            // [1 + 4*max_batch*nbands]
-    int *sync_aux[2] = {nullptr, nullptr};   // per internal stream (pipelined host entry)
-    cudaStream_t aux[2] = {nullptr, nullptr};
-    cudaEvent_t ev_start = nullptr, ev_aux[2] = {nullptr, nullptr};
+    // pipelined host entry point: copy-in stream, two compute streams, copy-out stream
+    int *sync_aux[2] = {nullptr, nullptr};   // sweep sync buffers per compute stream
+    cudaStream_t aux[4] = {nullptr, nullptr, nullptr, nullptr};   // h2d, comp0, comp1, d2h
+    cudaEvent_t ev_start = nullptr, ev_aux[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t *ev_in = nullptr, *ev_comp = nullptr;             // per chunk
+    int nchunk_ev = 0;
     // staging for the _host entry point (device)
     uint8_t *img_stage = nullptr;   // [max_batch][4][H][pitch]
     long long stage_pitch = 0;
@@ -80,6 +83,12 @@ void free_all(sgm_handle *h) {
     if (h->ev_start) cudaEventDestroy(h->ev_start);
     for (auto &e : h->ev_aux)
         if (e) cudaEventDestroy(e);
+    for (int k = 0; k < h->nchunk_ev; ++k) {
+        if (h->ev_in && h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
+        if (h->ev_comp && h->ev_comp[k]) cudaEventDestroy(h->ev_comp[k]);
+    }
+    delete[] h->ev_in;
+    delete[] h->ev_comp;
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
 }
@@ -174,8 +183,16 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     if (e == cudaSuccess) e = dalloc(&h->gbuf, nv * size_t(h->nbands) * size_t(W) * 3 * size_t(h->dp));
     if (e == cudaSuccess) e = dalloc(&h->sync, 1 + nv * size_t(h->nbands));
     for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = dalloc(&h->sync_aux[k], 1 + nv * size_t(h->nbands));
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamCreateWithFlags(&h->aux[k], cudaStreamNonBlocking);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&h->ev_aux[k], cudaEventDisableTiming);
+    for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaStreamCreateWithFlags(&h->aux[k], cudaStreamNonBlocking);
+    for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&h->ev_aux[k], cudaEventDisableTiming);
+    h->nchunk_ev = p->max_batch;
+    h->ev_in = new (std::nothrow) cudaEvent_t[h->nchunk_ev]();
+    h->ev_comp = new (std::nothrow) cudaEvent_t[h->nchunk_ev]();
+    if (!h->ev_in || !h->ev_comp) e = cudaErrorMemoryAllocation;
+    for (int k = 0; k < h->nchunk_ev && e == cudaSuccess; ++k) {
+        e = cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_comp[k], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
     if (e == cudaSuccess) e = dalloc(&h->img_stage, nv * size_t(H) * size_t(h->stage_pitch));
     if (e == cudaSuccess) e = dalloc(&h->flow_stage, size_t(p->max_batch) * npx * 2);
@@ -461,30 +478,35 @@ sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, 
     const int W = h->prm.width, H = h->prm.height;
     const long long npx = h->npx;
     const bool want_disp = out->disp_int || out->disp_sub || out->disp_valid;
-    // Pipeline over chunks of quads on two internal streams: the host->device copy of
-    // chunk c+1 and the device->host copy of chunk c-1 overlap the kernels of chunk c
-    // (the copy engines run beside the SMs; each stream has its own sweep sync buffers).
+    // Pipeline over chunks of quads: one stream copies every chunk's inputs in, two
+    // compute streams take alternate chunks as soon as their inputs have landed (so the
+    // sweeps of neighbouring chunks overlap on the SMs), one stream copies each chunk's
+    // results out as soon as it is done.  Each compute stream has its own sweep sync
+    // buffers.  The caller's stream orders the whole thing before and after.
     const int chunk = n >= 4 ? 2 : n;
+    cudaStream_t sin = h->aux[0], sout = h->aux[3];
     const bool timing = h->timing;
     h->timing = false;
     cudaError_t e = cudaEventRecord(h->ev_start, st);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(h->aux[k], h->ev_start, 0);
+    for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(h->aux[k], h->ev_start, 0);
     sgm_status s = SGM_OK;
     int c = 0;
     for (int q0 = 0; q0 < n && e == cudaSuccess && s == SGM_OK; q0 += chunk, ++c) {
         const int cq = n - q0 < chunk ? n - q0 : chunk;
-        cudaStream_t cs = h->aux[c & 1];
+        cudaStream_t cs = h->aux[1 + (c & 1)];
         uint8_t *img_dev = h->img_stage + 4LL * q0 * H * h->stage_pitch;
         float *flow_dev = h->flow_stage + 2LL * q0 * npx;
         uint8_t *fv_dev = h->fvalid_stage + (long long)q0 * npx;
         e = cudaMemcpy2DAsync(img_dev, size_t(h->stage_pitch), images + 4LL * q0 * H * W, size_t(W),
-                              size_t(W), size_t(4LL * cq * H), cudaMemcpyHostToDevice, cs);
+                              size_t(W), size_t(4LL * cq * H), cudaMemcpyHostToDevice, sin);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(flow_dev, flow + 2LL * q0 * npx, sizeof(float) * 2 * npx * cq,
-                                cudaMemcpyHostToDevice, cs);
+                                cudaMemcpyHostToDevice, sin);
         if (e == cudaSuccess && flow_valid)
             e = cudaMemcpyAsync(fv_dev, flow_valid + (long long)q0 * npx, size_t(npx) * cq,
-                                cudaMemcpyHostToDevice, cs);
+                                cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) e = cudaEventRecord(h->ev_in[c], sin);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, h->ev_in[c], 0);
         if (e != cudaSuccess) break;
         sgm_sceneflow_out dev{};
         dev.sf = h->sf_stage + 4LL * q0 * npx;
@@ -497,10 +519,12 @@ sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, 
         s = scene_flow_impl(h, cq, img_dev, h->stage_pitch, flow_dev, flow_valid ? fv_dev : nullptr,
                             cam, &dev, cs, q0, h->sync_aux[c & 1]);
         if (s != SGM_OK) break;
+        e = cudaEventRecord(h->ev_comp[c], cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, h->ev_comp[c], 0);
         auto d2h = [&](void *dst, const void *src, size_t bytes) {
-            if (dst && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs);
+            if (dst && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, sout);
         };
-        d2h(out->sf ? out->sf + 4LL * q0 * npx : nullptr, dev.sf, sizeof(float) * 4 * npx * cq);
+        d2h(out->sf + 4LL * q0 * npx, dev.sf, sizeof(float) * 4 * npx * cq);
         d2h(out->valid_sf + (long long)q0 * npx, dev.valid_sf, size_t(npx) * cq);
         if (want3d) {
             d2h(out->p0 + 4LL * q0 * npx, dev.p0, sizeof(float) * 4 * npx * cq);
@@ -514,8 +538,8 @@ sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, 
             d2h(out->disp_valid ? out->disp_valid + o : nullptr, h->lr_valid + o, size_t(2 * npx) * cq);
         }
     }
-    // the caller's stream waits for both internal streams
-    for (int k = 0; k < 2; ++k) {
+    // the caller's stream waits for every internal stream
+    for (int k = 0; k < 4; ++k) {
         cudaError_t e2 = cudaEventRecord(h->ev_aux[k], h->aux[k]);
         if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, h->ev_aux[k], 0);
         if (e == cudaSuccess) e = e2;
