@@ -317,36 +317,45 @@ def main():
                         "algorithmic_bytes_per_launch": sweep_bytes_per_cell(True) * view_cells}}
 
     # ---------------- e2e through the public API with host buffers
+    # Every step uploads its own inputs from pinned host memory and downloads its result
+    # (S + mask, 3D motion dP + mask) through sgm_scene_flow_host; steps are issued back
+    # to back (two alternating host buffer sets), so step k+1's upload and step k-1's
+    # download overlap step k's kernels; the span of the K steps is timed on the stream.
     e2e = None
     if not args.no_e2e:
-        himg = torch.from_numpy(np.stack([[q[k] for k in ("il0", "ir0", "il1", "ir1")]
-                                          for q in quads])).pin_memory()
-        hflow = torch.from_numpy(np.stack([q["flow"] for q in quads])).pin_memory()
-        hout = sgm.alloc_outputs(F, with_disp=False, pinned_host=True)
-        h2d = himg.numel() + hflow.numel() * 4
-        d2h = sum(t.numel() * t.element_size() for t in hout.values())
+        sets = []
+        for _ in range(2):
+            himg = torch.from_numpy(np.stack([[q[k] for k in ("il0", "ir0", "il1", "ir1")]
+                                              for q in quads])).pin_memory()
+            hflow = torch.from_numpy(np.stack([q["flow"] for q in quads])).pin_memory()
+            hout = sgm.alloc_outputs(F, with_disp=False, pinned_host=True, with_p0=False)
+            sets.append((himg, hflow, hout))
+        h2d = sets[0][0].numel() + sets[0][1].numel() * 4
+        d2h = sum(t.numel() * t.element_size() for t in sets[0][2].values())
         sgm.set_timing(False)
         with torch.cuda.stream(stream):
-            for _ in range(max(args.warmup, 3)):
+            for k in range(max(args.warmup, 3)):
+                himg, hflow, hout = sets[k & 1]
                 sgm.scene_flow_host(himg, hflow, cam, hout, stream=stream)
             stream.synchronize()
             if pg is not None:
                 dist.barrier()
-            tot = 0.0
-            for _ in range(args.steps):
-                flush.fill_(1)
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for k in range(args.steps):
+                himg, hflow, hout = sets[k & 1]
                 sgm.scene_flow_host(himg, hflow, cam, hout, stream=stream)
-                e1.record(stream)
-                e1.synchronize()
-                tot += e0.elapsed_time(e1)
+            e1.record(stream)
+            e1.synchronize()
+            tot = e0.elapsed_time(e1)
         tot = max_over_ranks(tot, dev)
         e2e_ms = tot / args.steps
         e2e = {"value": maps * W * H * D / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e2e_ms, "frames_per_s": F * world / (e2e_ms * 1e-3)}
+               "ms_per_step": e2e_ms, "frames_per_s": F * world / (e2e_ms * 1e-3),
+               "pipelined": "steps issued back to back; per-step upload/download overlap the "
+                            "neighbouring steps' kernels"}
 
     gather = None
     if args.gather and pg is not None:

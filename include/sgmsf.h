@@ -81,9 +81,10 @@ typedef struct sgm_handle sgm_handle;
 typedef struct sgm_sceneflow_out {
     float   *sf;            /* [n][H][W][4] = (u, v, d0, d1) (Eq. (3)); 0 where invalid */
     uint8_t *valid_sf;      /* [n][H][W] 1 = S(x) defined (Eq. (4)) */
-    float   *p0;            /* [n][H][W][4] = (X, Y, Z, 0) of x at t (NULL: skip 3D) */
+    float   *p0;            /* [n][H][W][4] = (X, Y, Z, 0) of x at t (NULL: not stored) */
     float   *dp;            /* [n][H][W][4] = (dX, dY, dZ, 0) motion (NULL: skip 3D) */
-    uint8_t *valid_3d;      /* [n][H][W] 1 = S valid and d0 > 0 and d1 > 0 (G21) */
+    uint8_t *valid_3d;      /* [n][H][W] 1 = S valid and d0 > 0 and d1 > 0 (G21); required
+                               with dp */
     int16_t *disp_int;      /* [n][2][H][W] LR-checked integer D0 (t), D1 (t+1) */
     float   *disp_sub;      /* [n][2][H][W] LR-checked sub-pixel D0, D1 (-1 invalid) */
     uint8_t *disp_valid;    /* [n][2][H][W] LR masks of D0, D1 */
@@ -164,7 +165,8 @@ SGM_API sgm_status sgm_disparity(sgm_handle *h, const uint8_t *left, const uint8
  *   valid_3d = valid_sf and d0 > 0 and d1 > 0.
  * d0, d1 [H][W] float32 (LR-checked sub-pixel maps at t, t+1); v0, v1 [H][W]
  * uint8; flow [H][W][2] float32 (u, v); flow_valid nullable (all valid, G23);
- * sf [H][W][4]; p0, dp [H][W][4] nullable (skip 3D; then valid_3d may be NULL).
+ * sf [H][W][4]; dp [H][W][4] nullable (skip 3D; then valid_3d may be NULL); p0
+ * [H][W][4] nullable (P0 is still computed for dp but not stored).
  */
 SGM_API sgm_status sgm_combine_sceneflow(sgm_handle *h, const float *d0, const uint8_t *v0,
                                  const float *d1, const uint8_t *v1, const float *flow,
@@ -183,11 +185,16 @@ SGM_API sgm_status sgm_scene_flow(sgm_handle *h, int32_t n, const uint8_t *image
                           const sgm_camera *cam, const sgm_sceneflow_out *out, void *stream);
 
 /* Same as sgm_scene_flow but every buffer (inputs and the non-NULL outputs of
- * *out) is HOST memory, densely packed ([n][4][H][W] images): the call
- * enqueues host->device copies into the handle's staging buffers, the
- * pipeline, and device->host copies of the requested outputs on `stream`.
- * Use page-locked host memory for asynchronous copies; the results are
- * available after the caller synchronises `stream`. */
+ * *out) is HOST memory, densely packed ([n][4][H][W] images).  The call enqueues,
+ * on internal streams of the handle, a 1D host->device copy into one of two
+ * staging slots, the pipeline, and device->host copies of the requested outputs,
+ * then makes `stream` wait for the copies; the results are available after the
+ * caller synchronises `stream`.  Consecutive host-entry calls on a handle are
+ * ordered among themselves through the slots' events, not through `stream`, so
+ * calls issued back to back pipeline: the upload of call k+1 and the download of
+ * call k-1 overlap the kernels of call k.  Use page-locked host memory, keep the
+ * host buffers of a call untouched until its results are available, and do not
+ * interleave other entry points of the same handle without synchronising. */
 SGM_API sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images,
                                const float *flow, const uint8_t *flow_valid,
                                const sgm_camera *cam, const sgm_sceneflow_out *out,

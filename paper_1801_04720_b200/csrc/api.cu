@@ -33,19 +33,23 @@ struct sgm_handle {
     uint8_t *lr_valid = nullptr;
     uint16_t *gbuf = nullptr;       // [4*max_batch][nbands][W][3][Dp]
     int *sync = nullptr;            // [1 + 4*max_batch*nbands]
-    // pipelined host entry point: copy-in stream, two compute streams, copy-out stream
-    int *sync_aux[2] = {nullptr, nullptr};   // sweep sync buffers per compute stream
-    cudaStream_t aux[4] = {nullptr, nullptr, nullptr, nullptr};   // h2d, comp0, comp1, d2h
-    cudaEvent_t ev_start = nullptr, ev_aux[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t *ev_in = nullptr, *ev_comp = nullptr;             // per chunk
-    int nchunk_ev = 0;
-    // staging for the _host entry point (device)
-    uint8_t *img_stage = nullptr;   // [max_batch][4][H][pitch]
+    // staging for the _host entry point (device): two slots so that back-to-back calls
+    // pipeline (upload of call k+1 and download of call k-1 overlap the kernels of call k)
     long long stage_pitch = 0;
-    float *flow_stage = nullptr;    // [max_batch][H][W][2]
-    uint8_t *fvalid_stage = nullptr;
-    float *sf_stage = nullptr, *p0_stage = nullptr, *dp_stage = nullptr;
-    uint8_t *vsf_stage = nullptr, *v3_stage = nullptr;
+    struct Stage {
+        uint8_t *img_dense = nullptr;   // [max_batch][4][H][W] (1D host copy target)
+        uint8_t *img = nullptr;         // [max_batch][4][H][pitch]
+        float *flow = nullptr;          // [max_batch][H][W][2]
+        uint8_t *fvalid = nullptr;      // [max_batch][H][W]
+        float *sf = nullptr, *p0 = nullptr, *dp = nullptr;   // [max_batch][H][W][4]
+        uint8_t *vsf = nullptr, *v3 = nullptr;               // [max_batch][H][W]
+        int16_t *di = nullptr; float *ds = nullptr; uint8_t *dv = nullptr;   // [max_batch][2][H][W]
+        cudaEvent_t ev_in = nullptr, ev_comp = nullptr, ev_out = nullptr;
+        bool used = false;
+    } stage[2];
+    int slot = 0;
+    cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+    int *sync_host = nullptr;       // sweep sync buffer of the host entry's compute stream
     // instrumentation
     bool timing = false;
     bool timed = false;
@@ -73,28 +77,23 @@ cudaError_t dalloc(T **p, size_t count) {
 
 void free_all(sgm_handle *h) {
     void *ptrs[] = {h->census, h->sfwd, h->dint, h->dsub, h->lr_int, h->lr_sub, h->lr_valid,
-                    h->gbuf, h->sync, h->img_stage, h->flow_stage, h->fvalid_stage,
-                    h->sf_stage, h->p0_stage, h->dp_stage, h->vsf_stage, h->v3_stage,
-                    h->sync_aux[0], h->sync_aux[1]};
+                    h->gbuf, h->sync, h->sync_host};
     for (void *p : ptrs)
         if (p) cudaFree(p);
-    for (auto &s : h->aux)
-        if (s) cudaStreamDestroy(s);
-    if (h->ev_start) cudaEventDestroy(h->ev_start);
-    for (auto &e : h->ev_aux)
-        if (e) cudaEventDestroy(e);
-    for (int k = 0; k < h->nchunk_ev; ++k) {
-        if (h->ev_in && h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
-        if (h->ev_comp && h->ev_comp[k]) cudaEventDestroy(h->ev_comp[k]);
+    for (auto &st : h->stage) {
+        void *sp[] = {st.img_dense, st.img, st.flow, st.fvalid, st.sf, st.p0, st.dp, st.vsf, st.v3,
+                      st.di, st.ds, st.dv};
+        for (void *p : sp)
+            if (p) cudaFree(p);
+        for (cudaEvent_t e : {st.ev_in, st.ev_comp, st.ev_out})
+            if (e) cudaEventDestroy(e);
     }
-    delete[] h->ev_in;
-    delete[] h->ev_comp;
+    for (cudaStream_t s : {h->s_in, h->s_comp, h->s_out})
+        if (s) cudaStreamDestroy(s);
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
 }
 
-// Sweep parameters for `nviews` views starting at quad `qoff` of the handle's scratch,
-// synchronising through `sync` (ticket + per-band progress flags).
 sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int qoff = 0, int *sync = nullptr) {
     sgm::SweepParams p{};
     const long long v0 = 4LL * qoff;
@@ -182,26 +181,26 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     if (e == cudaSuccess) e = dalloc(&h->lr_valid, nv / 2 * npx);
     if (e == cudaSuccess) e = dalloc(&h->gbuf, nv * size_t(h->nbands) * size_t(W) * 3 * size_t(h->dp));
     if (e == cudaSuccess) e = dalloc(&h->sync, 1 + nv * size_t(h->nbands));
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = dalloc(&h->sync_aux[k], 1 + nv * size_t(h->nbands));
-    for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaStreamCreateWithFlags(&h->aux[k], cudaStreamNonBlocking);
-    for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&h->ev_aux[k], cudaEventDisableTiming);
-    h->nchunk_ev = p->max_batch;
-    h->ev_in = new (std::nothrow) cudaEvent_t[h->nchunk_ev]();
-    h->ev_comp = new (std::nothrow) cudaEvent_t[h->nchunk_ev]();
-    if (!h->ev_in || !h->ev_comp) e = cudaErrorMemoryAllocation;
-    for (int k = 0; k < h->nchunk_ev && e == cudaSuccess; ++k) {
-        e = cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_comp[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = dalloc(&h->sync_host, 1 + nv * size_t(h->nbands));
+    const size_t mb = size_t(p->max_batch);
+    for (auto &st : h->stage) {
+        if (e == cudaSuccess) e = dalloc(&st.img_dense, nv * size_t(H) * size_t(W));
+        if (e == cudaSuccess) e = dalloc(&st.img, nv * size_t(H) * size_t(h->stage_pitch));
+        if (e == cudaSuccess) e = dalloc(&st.flow, mb * npx * 2);
+        if (e == cudaSuccess) e = dalloc(&st.fvalid, mb * npx);
+        if (e == cudaSuccess) e = dalloc(&st.sf, mb * npx * 4);
+        if (e == cudaSuccess) e = dalloc(&st.p0, mb * npx * 4);
+        if (e == cudaSuccess) e = dalloc(&st.dp, mb * npx * 4);
+        if (e == cudaSuccess) e = dalloc(&st.vsf, mb * npx);
+        if (e == cudaSuccess) e = dalloc(&st.v3, mb * npx);
+        if (e == cudaSuccess) e = dalloc(&st.di, mb * npx * 2);
+        if (e == cudaSuccess) e = dalloc(&st.ds, mb * npx * 2);
+        if (e == cudaSuccess) e = dalloc(&st.dv, mb * npx * 2);
+        for (cudaEvent_t *ev : {&st.ev_in, &st.ev_comp, &st.ev_out})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     }
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = dalloc(&h->img_stage, nv * size_t(H) * size_t(h->stage_pitch));
-    if (e == cudaSuccess) e = dalloc(&h->flow_stage, size_t(p->max_batch) * npx * 2);
-    if (e == cudaSuccess) e = dalloc(&h->fvalid_stage, size_t(p->max_batch) * npx);
-    if (e == cudaSuccess) e = dalloc(&h->sf_stage, size_t(p->max_batch) * npx * 4);
-    if (e == cudaSuccess) e = dalloc(&h->p0_stage, size_t(p->max_batch) * npx * 4);
-    if (e == cudaSuccess) e = dalloc(&h->dp_stage, size_t(p->max_batch) * npx * 4);
-    if (e == cudaSuccess) e = dalloc(&h->vsf_stage, size_t(p->max_batch) * npx);
-    if (e == cudaSuccess) e = dalloc(&h->v3_stage, size_t(p->max_batch) * npx);
+    for (cudaStream_t *sp : {&h->s_in, &h->s_comp, &h->s_out})
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking);
     for (int i = 0; i <= SGM_NUM_STAGES && e == cudaSuccess; ++i) e = cudaEventCreate(&h->ev[i]);
     if (e == cudaSuccess) e = cudaMemset(h->sync, 0, sizeof(int) * (1 + nv * size_t(h->nbands)));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -370,7 +369,7 @@ sgm_status sgm_combine_sceneflow(sgm_handle *h, const float *d0, const uint8_t *
                                  uint8_t *valid_sf, uint8_t *valid_3d, void *stream) {
     if (!h || !d0 || !v0 || !d1 || !v1 || !flow || !sf || !valid_sf) return SGM_ERR_INVALID_ARGUMENT;
     const bool want3d = p0 || dp || valid_3d;
-    if (want3d && (!p0 || !dp || !valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
+    if (want3d && (!dp || !valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
     if (want3d && !(cam->f_px > 0.f && cam->baseline_m > 0.f)) return SGM_ERR_INVALID_ARGUMENT;
     if (!aligned16(sf) || (p0 && !aligned16(p0)) || (dp && !aligned16(dp)) ||
         (reinterpret_cast<uintptr_t>(flow) & 7))
@@ -383,7 +382,7 @@ sgm_status sgm_combine_sceneflow(sgm_handle *h, const float *d0, const uint8_t *
         p.f = cam->f_px; p.B = cam->baseline_m; p.cx = cam->cx; p.cy = cam->cy;
         p.fB = cam->f_px * cam->baseline_m;
     }
-    p.sf = sf; p.p0 = want3d ? p0 : nullptr; p.dp = dp; p.valid_sf = valid_sf; p.valid_3d = valid_3d;
+    p.sf = sf; p.p0 = p0; p.dp = want3d ? dp : nullptr; p.valid_sf = valid_sf; p.valid_3d = valid_3d;
     cudaError_t e = sgm::launch_combine(p, static_cast<cudaStream_t>(stream));
     if (e == cudaSuccess) ++h->launches;
     return from_cuda(e);
@@ -396,7 +395,7 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *image
     const int W = h->prm.width, H = h->prm.height;
     const long long npx = h->npx;
     const bool want3d = out->p0 || out->dp || out->valid_3d;
-    if (want3d && (!out->p0 || !out->dp || !out->valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
+    if (want3d && (!out->dp || !out->valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
     if (want3d && !(cam->f_px > 0.f && cam->baseline_m > 0.f)) return SGM_ERR_INVALID_ARGUMENT;
     const bool timing = h->timing;
     auto mark = [&](int i) {
@@ -444,7 +443,7 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *image
             p.fB = cam->f_px * cam->baseline_m;
         }
         p.sf = out->sf; p.valid_sf = out->valid_sf;
-        p.p0 = want3d ? out->p0 : nullptr; p.dp = out->dp; p.valid_3d = out->valid_3d;
+        p.p0 = out->p0; p.dp = want3d ? out->dp : nullptr; p.valid_3d = out->valid_3d;
         e = sgm::launch_combine(p, st);
         if (e != cudaSuccess) return from_cuda(e);
         ++h->launches;
@@ -473,79 +472,62 @@ sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, 
     if (!h || !images || !flow || !out || !out->sf || !out->valid_sf) return SGM_ERR_INVALID_ARGUMENT;
     if (n < 1 || n > h->prm.max_batch) return SGM_ERR_INVALID_ARGUMENT;
     const bool want3d = out->p0 || out->dp || out->valid_3d;
-    if (want3d && (!out->p0 || !out->dp || !out->valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
+    if (want3d && (!out->dp || !out->valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int W = h->prm.width, H = h->prm.height;
     const long long npx = h->npx;
-    const bool want_disp = out->disp_int || out->disp_sub || out->disp_valid;
-    // Pipeline over chunks of quads: one stream copies every chunk's inputs in, two
-    // compute streams take alternate chunks as soon as their inputs have landed (so the
-    // sweeps of neighbouring chunks overlap on the SMs), one stream copies each chunk's
-    // results out as soon as it is done.  Each compute stream has its own sweep sync
-    // buffers.  The caller's stream orders the whole thing before and after.
-    const int chunk = n >= 4 ? 2 : n;
-    cudaStream_t sin = h->aux[0], sout = h->aux[3];
+    // Three internal streams and two staging slots.  Call k uses slot k % 2:
+    //   copy-in  : wait until call k-2's kernels stopped reading the slot; 1D copies in
+    //   compute  : wait for the copy-in and for call k-2's copy-out of the slot; re-pitch,
+    //              census, sweeps, LR, combination (one launch set for the whole batch)
+    //   copy-out : wait for the compute; copy the requested results to the host
+    // and `stream` waits for the copy-out.  Calls issued back to back therefore overlap
+    // the upload of k+1 and the download of k-1 with the kernels of k.
+    sgm_handle::Stage &sg = h->stage[h->slot];
+    h->slot ^= 1;
     const bool timing = h->timing;
     h->timing = false;
-    cudaError_t e = cudaEventRecord(h->ev_start, st);
-    for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(h->aux[k], h->ev_start, 0);
-    sgm_status s = SGM_OK;
-    int c = 0;
-    for (int q0 = 0; q0 < n && e == cudaSuccess && s == SGM_OK; q0 += chunk, ++c) {
-        const int cq = n - q0 < chunk ? n - q0 : chunk;
-        cudaStream_t cs = h->aux[1 + (c & 1)];
-        uint8_t *img_dev = h->img_stage + 4LL * q0 * H * h->stage_pitch;
-        float *flow_dev = h->flow_stage + 2LL * q0 * npx;
-        uint8_t *fv_dev = h->fvalid_stage + (long long)q0 * npx;
-        e = cudaMemcpy2DAsync(img_dev, size_t(h->stage_pitch), images + 4LL * q0 * H * W, size_t(W),
-                              size_t(W), size_t(4LL * cq * H), cudaMemcpyHostToDevice, sin);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(flow_dev, flow + 2LL * q0 * npx, sizeof(float) * 2 * npx * cq,
-                                cudaMemcpyHostToDevice, sin);
-        if (e == cudaSuccess && flow_valid)
-            e = cudaMemcpyAsync(fv_dev, flow_valid + (long long)q0 * npx, size_t(npx) * cq,
-                                cudaMemcpyHostToDevice, sin);
-        if (e == cudaSuccess) e = cudaEventRecord(h->ev_in[c], sin);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, h->ev_in[c], 0);
-        if (e != cudaSuccess) break;
-        sgm_sceneflow_out dev{};
-        dev.sf = h->sf_stage + 4LL * q0 * npx;
-        dev.valid_sf = h->vsf_stage + (long long)q0 * npx;
-        if (want3d) {
-            dev.p0 = h->p0_stage + 4LL * q0 * npx;
-            dev.dp = h->dp_stage + 4LL * q0 * npx;
-            dev.valid_3d = h->v3_stage + (long long)q0 * npx;
-        }
-        s = scene_flow_impl(h, cq, img_dev, h->stage_pitch, flow_dev, flow_valid ? fv_dev : nullptr,
-                            cam, &dev, cs, q0, h->sync_aux[c & 1]);
-        if (s != SGM_OK) break;
-        e = cudaEventRecord(h->ev_comp[c], cs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, h->ev_comp[c], 0);
-        auto d2h = [&](void *dst, const void *src, size_t bytes) {
-            if (dst && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, sout);
-        };
-        d2h(out->sf + 4LL * q0 * npx, dev.sf, sizeof(float) * 4 * npx * cq);
-        d2h(out->valid_sf + (long long)q0 * npx, dev.valid_sf, size_t(npx) * cq);
-        if (want3d) {
-            d2h(out->p0 + 4LL * q0 * npx, dev.p0, sizeof(float) * 4 * npx * cq);
-            d2h(out->dp + 4LL * q0 * npx, dev.dp, sizeof(float) * 4 * npx * cq);
-            d2h(out->valid_3d + (long long)q0 * npx, dev.valid_3d, size_t(npx) * cq);
-        }
-        if (want_disp) {
-            const long long o = 2LL * q0 * npx;
-            d2h(out->disp_int ? out->disp_int + o : nullptr, h->lr_int + o, sizeof(int16_t) * 2 * npx * cq);
-            d2h(out->disp_sub ? out->disp_sub + o : nullptr, h->lr_sub + o, sizeof(float) * 2 * npx * cq);
-            d2h(out->disp_valid ? out->disp_valid + o : nullptr, h->lr_valid + o, size_t(2 * npx) * cq);
-        }
-    }
-    // the caller's stream waits for every internal stream
-    for (int k = 0; k < 4; ++k) {
-        cudaError_t e2 = cudaEventRecord(h->ev_aux[k], h->aux[k]);
-        if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, h->ev_aux[k], 0);
-        if (e == cudaSuccess) e = e2;
-    }
+    cudaError_t e = cudaSuccess;
+    if (sg.used) e = cudaStreamWaitEvent(h->s_in, sg.ev_comp, 0);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(sg.img_dense, images, size_t(4LL * n * H * W), cudaMemcpyHostToDevice, h->s_in);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(sg.flow, flow, sizeof(float) * 2 * npx * n, cudaMemcpyHostToDevice, h->s_in);
+    if (e == cudaSuccess && flow_valid)
+        e = cudaMemcpyAsync(sg.fvalid, flow_valid, size_t(npx) * n, cudaMemcpyHostToDevice, h->s_in);
+    if (e == cudaSuccess) e = cudaEventRecord(sg.ev_in, h->s_in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->s_comp, sg.ev_in, 0);
+    if (e == cudaSuccess && sg.used) e = cudaStreamWaitEvent(h->s_comp, sg.ev_out, 0);
+    if (e == cudaSuccess) e = sgm::launch_repitch(sg.img_dense, sg.img, W, h->stage_pitch, 4LL * n * H, h->s_comp);
+    if (e != cudaSuccess) { h->timing = timing; return from_cuda(e); }
+    ++h->launches;
+    sgm_sceneflow_out dev{};
+    dev.sf = sg.sf;
+    dev.valid_sf = sg.vsf;
+    if (want3d) { dev.p0 = out->p0 ? sg.p0 : nullptr; dev.dp = sg.dp; dev.valid_3d = sg.v3; }
+    dev.disp_int = sg.di; dev.disp_sub = sg.ds; dev.disp_valid = sg.dv;
+    sgm_status s = scene_flow_impl(h, n, sg.img, h->stage_pitch, sg.flow, flow_valid ? sg.fvalid : nullptr,
+                                   cam, &dev, h->s_comp, 0, h->sync_host);
     h->timing = timing;
     if (s != SGM_OK) return s;
+    sg.used = true;
+    e = cudaEventRecord(sg.ev_comp, h->s_comp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->s_out, sg.ev_comp, 0);
+    auto d2h = [&](void *dst, const void *src, size_t bytes) {
+        if (dst && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->s_out);
+    };
+    d2h(out->sf, sg.sf, sizeof(float) * 4 * npx * n);
+    d2h(out->valid_sf, sg.vsf, size_t(npx) * n);
+    if (want3d) {
+        d2h(out->p0, sg.p0, sizeof(float) * 4 * npx * n);
+        d2h(out->dp, sg.dp, sizeof(float) * 4 * npx * n);
+        d2h(out->valid_3d, sg.v3, size_t(npx) * n);
+    }
+    d2h(out->disp_int, sg.di, sizeof(int16_t) * 2 * npx * n);
+    d2h(out->disp_sub, sg.ds, sizeof(float) * 2 * npx * n);
+    d2h(out->disp_valid, sg.dv, size_t(2 * npx) * n);
+    if (e == cudaSuccess) e = cudaEventRecord(sg.ev_out, h->s_out);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, sg.ev_out, 0);
     return from_cuda(e);
 }
 

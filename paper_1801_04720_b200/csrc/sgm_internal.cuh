@@ -81,6 +81,8 @@ cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool 
 cudaError_t launch_wta(const uint16_t *agg, int W, int H, int D, int16_t *dint, float *dsub,
                        cudaStream_t st);
 cudaError_t launch_lr(const LrParams &p, cudaStream_t st);
+cudaError_t launch_repitch(const uint8_t *src, uint8_t *dst, int W, long long pitch, long long rows,
+                           cudaStream_t st);
 cudaError_t launch_combine(const CombineParams &p, cudaStream_t st);
 
 }  // namespace sgm

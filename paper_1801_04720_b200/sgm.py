@@ -164,7 +164,7 @@ class SGM:
         return {"sf": sf, "valid_sf": vsf, "p0": p0, "dp": dp, "valid_3d": v3}
 
     # ------------------------------------------------------------------ production path
-    def alloc_outputs(self, n, with_3d=True, with_disp=True, pinned_host=False):
+    def alloc_outputs(self, n, with_3d=True, with_disp=True, pinned_host=False, with_p0=True):
         H, W = self.H, self.W
         if pinned_host:
             mk = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True)  # noqa: E731
@@ -172,8 +172,9 @@ class SGM:
             mk = lambda shape, dt: self._empty(shape, dt)  # noqa: E731
         out = {"sf": mk((n, H, W, 4), torch.float32), "valid_sf": mk((n, H, W), torch.uint8)}
         if with_3d:
-            out.update(p0=mk((n, H, W, 4), torch.float32), dp=mk((n, H, W, 4), torch.float32),
-                       valid_3d=mk((n, H, W), torch.uint8))
+            out.update(dp=mk((n, H, W, 4), torch.float32), valid_3d=mk((n, H, W), torch.uint8))
+            if with_p0:
+                out["p0"] = mk((n, H, W, 4), torch.float32)
         if with_disp:
             out.update(disp_int=mk((n, 2, H, W), torch.int16),
                        disp_sub=mk((n, 2, H, W), torch.float32),

@@ -276,6 +276,21 @@ def test_host_entry_point_matches_device(dev):
     torch.cuda.synchronize()
     for k in hout:
         assert torch.equal(hout[k], ref[k].cpu()), k
+    # back-to-back calls pipeline through the two staging slots: three calls with
+    # different inputs, one synchronisation, every output intact
+    sets = []
+    for sel in ([0, 1], [2, 3], [4, 0]):
+        hi = torch.from_numpy(np.stack([[quads[i][k] for k in ("il0", "ir0", "il1", "ir1")]
+                                        for i in sel])).pin_memory()
+        hf = torch.from_numpy(np.stack([quads[i]["flow"] for i in sel])).pin_memory()
+        ho = g.alloc_outputs(2, pinned_host=True, with_p0=False)
+        g.scene_flow_host(hi, hf, cam, ho)
+        sets.append((sel, ho))
+    torch.cuda.synchronize()
+    for sel, ho in sets:
+        for j, i in enumerate(sel):
+            for k in ho:
+                assert torch.equal(ho[k][j], ref[k][i].cpu()), (sel, k)
     g.close()
 
 

@@ -10,8 +10,8 @@ quads = [synth.make_quad(cfg, i) for i in range(8)]
 g8 = SGM.from_config(cfg, max_batch=8)
 imgs, flow = stack_quads(quads, g8.pitch, dev)
 out8 = g8.alloc_outputs(8)
-gs = [SGM.from_config(cfg, max_batch=2) for _ in range(4)]
-outs = [g.alloc_outputs(2) for g in gs]
+gs = [SGM.from_config(cfg, max_batch=4) for _ in range(4)]
+outs = [g.alloc_outputs(4) for g in gs]
 streams = [torch.cuda.Stream() for _ in range(4)]
 def t(fn, reps=5):
     for _ in range(2): fn()
@@ -22,13 +22,14 @@ def t(fn, reps=5):
     e1.record(); e1.synchronize()
     return e0.elapsed_time(e1) / reps
 def one8(): g8.scene_flow(imgs, flow, cam, out8)
-def chunks(nstreams):
+def chunks(nstreams, cq=2):
     def f():
         cur = torch.cuda.current_stream()
         ev = torch.cuda.Event(); ev.record(cur)
-        for c in range(4):
+        for c in range(8 // cq):
             s = streams[c % nstreams]; s.wait_event(ev)
-            gs[c].scene_flow(imgs[2*c:2*c+2], flow[2*c:2*c+2], cam, outs[c], stream=s)
+            o = {k: v[:cq] for k, v in outs[c].items()}
+            gs[c].scene_flow(imgs[cq*c:cq*c+cq], flow[cq*c:cq*c+cq], cam, o, stream=s)
         for c in range(nstreams):
             cur.wait_stream(streams[c])
     return f
@@ -37,4 +38,5 @@ print("4 x 2 quads, 1 stream: %.2f ms" % t(chunks(1)))
 print("4 x 2 quads, 2 streams: %.2f ms" % t(chunks(2)))
 print("4 x 2 quads, 4 streams: %.2f ms" % t(chunks(4)))
 g1 = SGM.from_config(cfg, max_batch=1); o1 = g1.alloc_outputs(1)
-print("1 quad latency: %.2f ms" % t(lambda: g1.scene_flow(imgs[:1], flow[:1], cam, o1)))
+print("2 x 4 quads, 2 streams: %.2f ms" % t(chunks(2, 4)))
+print("[3,3,2] n/a; 1 quad latency: %.2f ms" % t(lambda: g1.scene_flow(imgs[:1], flow[:1], cam, o1)))
