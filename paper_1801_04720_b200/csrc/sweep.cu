@@ -114,21 +114,28 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
-// One semi-global path update for the CPL cells a lane holds.
-//   prev: L_r(p - r, .) (u16x2 pairs), C: C(p, .), out: L_r(p, .).
+// One semi-global path update for the CPL cells a lane holds, on path vectors
+// carried with a +P1 bias (Lb = L + P1, u16x2 pairs):
+//   t  = min(L(d-1) + P1, L(d+1) + P1, L(d), m + P2)      (exactly the recursion's min term)
+//      = VIMNMX3(Lb(d-1), Lb(d+1), VIADDMNMX(Lb(d), -P1, m + P2))
+//   Lb'(d) = C(d) + t - m + P1,   m = min_k L(p - r, k) = min_k Lb - P1.
+// The bias turns the three min operations per pair of the plain form into two (the +P1
+// of the neighbours is already in their stored value).  A path start is the vector P1
+// (L = 0, m = 0), which returns Lb' = C + P1.
 //   sel_up / sel_dn: PRMT selectors building the d-1 / d+1 neighbour pairs (per lane).
 template <int R>
 __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uint32_t (&C)[R],
-                                            uint32_t (&out)[R], uint32_t p1x2, uint32_t p2x2,
-                                            uint32_t sel_up, uint32_t sel_dn, uint32_t one) {
-    // m = min_k L_r(p - r, k): min over the lane's pairs, then over the two halves (the
+                                            uint32_t (&out)[R], uint32_t negp1x2, uint32_t p2mp1x2,
+                                            uint32_t twop1x2, uint32_t sel_up, uint32_t sel_dn) {
+    // mb = min_k Lb(p - r, k): min over the lane's pairs, then over the two halves (the
     // high half is brought down with IMAD.HI on the FMA pipe), then over the warp
     uint32_t v = prev[0];
 #pragma unroll
     for (int r = 1; r < R; ++r) v = __vminu2(v, prev[r]);
     v = __vminu2(v, __umulhi(v, 0x10000u));           // lo = min(lo, hi), hi = 0
-    const uint32_t m = __reduce_min_sync(0xffffffffu, v);
-    const uint32_t mP2 = imad(m, 0x10001u, p2x2);     // m + P2 in both halves
+    const uint32_t mb = __reduce_min_sync(0xffffffffu, v);
+    const uint32_t mP2 = imad(mb, 0x10001u, p2mp1x2);  // m + P2 = mb - P1 + P2, both halves
+    const uint32_t K = imad(mb, 0xFFFEFFFFu, twop1x2); // 2 P1 - mb in both halves (mod 2^32)
     // neighbours d-1 / d+1
     const uint32_t up = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
     const uint32_t dn = __shfl_down_sync(0xffffffffu, prev[0], 1);
@@ -139,11 +146,10 @@ __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uin
     nb[R] = __byte_perm(prev[R - 1], dn, sel_dn);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        uint32_t t = __vminu2(nb[r], nb[r + 1]);       // min(L(d-1), L(d+1))
-        t = __viaddmin_u16x2(t, p1x2, prev[r]);        // min(.. + P1, L(d))
-        t = __vminu2(t, mP2);                          // min(.., m + P2)
-        // + C - m in both halves: exact mod 2^32 since each half's result is in [0, 2^16)
-        out[r] = t + C[r] - m * 0x10001u;
+        const uint32_t centre = __viaddmin_u16x2(prev[r], negp1x2, mP2);   // min(L(d), m + P2)
+        const uint32_t t = __vimin3_u16x2(nb[r], nb[r + 1], centre);
+        // C + t - m + P1: exact mod 2^32, every half's result lies in [P1, 2^16)
+        out[r] = t + C[r] + K;
     }
 }
 
@@ -223,7 +229,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     {
         uint4 *z = reinterpret_cast<uint4 *>(smem_raw);
         const int n16 = int((size_t(NW) * RS + kRing0) * VEC * 2 / 16);
-        for (int k = threadIdx.x; k < n16; k += (NW + 1) * 32) z[k] = make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t ps = uint32_t(p.P1) * 0x10001u;     // biased path-start vector
+        for (int k = threadIdx.x; k < n16; k += (NW + 1) * 32) z[k] = make_uint4(ps, ps, ps, ps);
     }
     __shared__ int s_ticket;
     if (threadIdx.x < 2 * NW * RG) mbar_init(bars + threadIdx.x, 32);
@@ -294,7 +301,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     // per-lane constants
     const uint32_t one = uint32_t(p.one);
     const uint32_t p1x2 = uint32_t(p.P1) * 0x10001u;
-    const uint32_t p2x2 = uint32_t(p.P2) * 0x10001u;
+    const uint32_t negp1x2 = (uint32_t(0x10000 - p.P1) & 0xFFFFu) * 0x10001u;   // -P1 per half
+    const uint32_t p2mp1x2 = uint32_t(p.P2 - p.P1) * 0x10001u;                  // P2 - P1
+    const uint32_t twop1x2 = 2u * p1x2;
+    const uint32_t negb4 = 0u - 4u * p1x2;            // removes the 4 path biases from S
     const int dbase = CPL * lane;
     const bool has_pad = p.D < DP;
     // PRMT selectors for the d-1 / d+1 neighbour pairs: at d = 0 (lane 0) the missing d-1
@@ -387,7 +397,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     // state
     uint32_t Lh[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) Lh[r] = 0;
+    for (int r = 0; r < R; ++r) Lh[r] = p1x2;                // path start (biased zero)
     using CW = typename std::conditional<C64, uint64_t, uint32_t>::type;
     CW win[CPL];
 #pragma unroll
@@ -520,17 +530,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             uint32_t S[R];
             {
                 uint32_t nL[R];
-                path_update<R>(Lh, C, nL, p1x2, p2x2, sel_up, sel_dn, one);
+                path_update<R>(Lh, C, nL, negp1x2, p2mp1x2, twop1x2, sel_up, sel_dn);
 #pragma unroll
                 for (int r = 0; r < R; ++r) { Lh[r] = nL[r]; S[r] = nL[r]; }
             }
             uint32_t nv[3][R];
 #pragma unroll
-            for (int v = 0; v < 3; ++v) {
-                path_update<R>(pv[v], C, nv[v], p1x2, p2x2, sel_up, sel_dn, one);
+            for (int v = 0; v < 3; ++v)
+                path_update<R>(pv[v], C, nv[v], negp1x2, p2mp1x2, twop1x2, sel_up, sel_dn);
+            // S = sum of the four unbiased path costs: the -4 P1 rides in IADD3's third slot
 #pragma unroll
-                for (int r = 0; r < R; ++r) S[r] += nv[v][r];
-            }
+            for (int r = 0; r < R; ++r) S[r] = (S[r] + nv[0][r] + nv[1][r]) + (nv[2][r] + negb4);
             // --- hand the three vectors to the row below
             if (has_row_below) {
                 if ((ph % G) == G - 1) {                   // next group's slots free again?
@@ -545,7 +555,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                 uint16_t *g = gout + (long long)i * VEC;
                 uint32_t zero[R];
 #pragma unroll
-                for (int r = 0; r < R; ++r) zero[r] = 0;
+                for (int r = 0; r < R; ++r) zero[r] = p1x2;        // biased path start
                 VecIO<R>::st(g, nv[0]);
                 if (i + 1 < W) VecIO<R>::st(g + VEC + DP, nv[1]);
                 if (i > 0) VecIO<R>::st(g - VEC + 2 * DP, nv[2]);
@@ -631,7 +641,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
         // x' = W-1, so that slot's v2 must read as zero; then release slot W-1.
         uint32_t zero[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) zero[r] = 0;
+        for (int r = 0; r < R; ++r) zero[r] = p1x2;                // biased path start
         VecIO<R>::st(my_ring + size_t((W - 1) & (RS - 1)) * VEC + 2 * DP, zero);
         mbar_arrive(my_full + (((W - 1) / G) % RG));
     }
