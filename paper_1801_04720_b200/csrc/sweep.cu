@@ -402,12 +402,18 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     CW win[CPL];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) win[k] = 0;
-    uint32_t pf[2][R];                               // BWD: S_fwd prefetch (2 positions)
+    // BWD: S_fwd register prefetch PF positions ahead (slot = position mod PF must be a
+    // compile-time index, so PF divides the unroll CPL)
+    constexpr int PF = (CPL % 4 == 0) ? 4 : 2;
+    uint32_t pf[PF][R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) { pf[0][r] = 0; pf[1][r] = 0; }
+    for (int k = 0; k < PF; ++k)
+#pragma unroll
+        for (int r = 0; r < R; ++r) pf[k][r] = 0;
     if (BWD) {
-        VecIO<R>::ld(sfwd_ptr, pf[0]);
-        if (W > 1) VecIO<R>::ld(sfwd_ptr + sstep, pf[1]);
+#pragma unroll
+        for (int k = 0; k < PF; ++k)
+            if (k < W) VecIO<R>::ld(sfwd_ptr + k * sstep, pf[k]);
     }
     uint32_t rec_key = 0, rec_ac = 0;                // BWD: WTA record of position (i & ~31) + lane
     const bool do_wta = BWD && p.dint != nullptr;
@@ -482,14 +488,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             // (C_max + P2) <= 1020 < 2^10, C <= C_max <= 63 < 2^6; sgm_create enforces both).
             uint32_t C[R], craw[R], Sf[R];
             if (BWD) {
-                const int slot = ph & 1;
+                const int slot = ph % PF;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     craw[r] = pf[slot][r] & 0x003F003Fu;
                     Sf[r] = (pf[slot][r] >> 6) & 0x03FF03FFu;
                     C[r] = craw[r] + pad[r];
                 }
-                if (i + 2 < W) VecIO<R>::ld(sfwd_ptr + 2 * sstep, pf[slot]);
+                if (i + PF < W) VecIO<R>::ld(sfwd_ptr + PF * sstep, pf[slot]);
                 sfwd_ptr += sstep;
             } else {
                 const uint64_t rv = cref[i & 63];
