@@ -453,8 +453,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             // --- census prefetch refill
             if (BWD) {
             } else if ((i & 31) == 0) {
-                const int q = i + 32 + lane;
-                if (q < W) {
+                const int q = min(i + 32 + lane, W - 1);   // clamped: keeps the loads unpredicated
+                {
                     const int xq = xview(q);
                     int xm = xq - (BWD ? DP - 1 : 0);
                     xm = xm < 0 ? 0 : xm;
@@ -495,7 +495,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                     Sf[r] = (pf[slot][r] >> 6) & 0x03FF03FFu;
                     C[r] = craw[r] + pad[r];
                 }
-                if (i + PF < W) VecIO<R>::ld(sfwd_ptr + PF * sstep, pf[slot]);
+                // unconditional load (clamped to the last position): a predicated load would
+                // make the compiler copy the result into the slot at once and stall on it
+                VecIO<R>::ld(sfwd_ptr + (i + PF < W ? PF : W - 1 - i) * sstep, pf[slot]);
                 sfwd_ptr += sstep;
             } else {
                 const uint64_t rv = cref[i & 63];
