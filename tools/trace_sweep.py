@@ -49,3 +49,26 @@ for tt in np.linspace(0, en[valid].max(), 20):
 print("resident CTAs over time:", conc)
 sm = t[:, 0, 2].astype(int)
 print("distinct SMs used:", len(set(sm.tolist())))
+# --- per-CTA span vs per-warp work, per-row start lag, band start lag
+span = en.max(axis=1) - st.min(axis=1)
+print(f"CTA span median {np.median(span):.1f} us; warp loop median {np.median(dur[valid]):.1f} us")
+rowlag = np.diff(st, axis=1)[:, :]
+print(f"per-row start lag median {np.median(rowlag):.2f} us = {np.median(rowlag) * 1e3 / (np.median(dur[valid]) * 1e3 / cfg.W):.1f} positions")
+nv = 4 * F
+bandstart = st[:, 0].reshape(-1, nv)   # [band][view]
+bl = np.diff(bandstart, axis=0)
+print(f"band-to-band start lag median {np.median(bl):.2f} us")
+# time when each SM was busy: union of CTA spans per SM
+busy = 0.0
+sms = t[:, 0, 2].astype(int)
+for smid in set(sms.tolist()):
+    iv = sorted(zip(st.min(axis=1)[sms == smid], en.max(axis=1)[sms == smid]))
+    cur_s, cur_e = iv[0]
+    for a, b in iv[1:]:
+        if a > cur_e:
+            busy += cur_e - cur_s
+            cur_s, cur_e = a, b
+        else:
+            cur_e = max(cur_e, b)
+    busy += cur_e - cur_s
+print(f"SM busy fraction over the kernel span: {busy / (len(set(sms.tolist())) * en[valid].max()):.3f}")
