@@ -55,9 +55,10 @@ def _get():
                                           P, P, P, P, P, P, P]
             lib.orc_combine.argtypes = [P, P, P, P, P, P, I, I, I, P, P]
             lib.orc_reproject.argtypes = [P, P, I, I, Dd, Dd, Dd, Dd, P, P, P, P]
+            lib.orc_evaluate.argtypes = [P, P, P, P, P, P, P, I, I, ctypes.c_float, ctypes.c_float, P]
             for fn in ("orc_census", "orc_cost", "orc_path", "orc_aggregate", "orc_wta",
                        "orc_lr_check", "orc_sgm_view", "orc_disparity", "orc_combine",
-                       "orc_reproject"):
+                       "orc_reproject", "orc_evaluate"):
                 getattr(lib, fn).restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -188,6 +189,24 @@ def reproject(sf, valid_sf, f, B, cx, cy):
     _chk(_get().orc_reproject(_p(sf), _p(valid_sf), W, H, f, B, cx, cy,
                               _p(p0), _p(p1), _p(dp), _p(v3)), "reproject")
     return p0, p1, dp, v3
+
+
+def evaluate(sf, valid_sf, gt_d0, gt_d1, gt_flow, gt_noc, gt_valid=None, tau_abs=3.0,
+             tau_rel=0.05):
+    """KITTI-style outlier counts (float32 decisions).  Returns int64 [2][6] =
+    {n_gt, n_eval, n_d1, n_d2, n_fl, n_sf} for split 0 (all) and 1 (non-occluded)."""
+    sf = _c(sf, np.float32)
+    valid_sf = _c(valid_sf, np.uint8)
+    gt_d0 = _c(gt_d0, np.float32)
+    gt_d1 = _c(gt_d1, np.float32)
+    gt_flow = _c(gt_flow, np.float32)
+    gt_noc = _c(gt_noc, np.uint8)
+    gv = None if gt_valid is None else _c(gt_valid, np.uint8)
+    H, W = valid_sf.shape
+    out = np.zeros((2, 6), np.int64)
+    _chk(_get().orc_evaluate(_p(sf), _p(valid_sf), _p(gt_d0), _p(gt_d1), _p(gt_flow), _p(gv),
+                             _p(gt_noc), W, H, tau_abs, tau_rel, _p(out)), "evaluate")
+    return out
 
 
 def run_quad(quad, prm, rule=0, threads=True):

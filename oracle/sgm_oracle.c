@@ -384,3 +384,63 @@ int orc_reproject(const double *sf, const uint8_t *valid_sf, int W, int H,
         }
     return 0;
 }
+
+/* ------------------------------------------------------------------ */
+/* Evaluation (SPEC eval S:449-499; Table 1      */
+/* semantics P:130-155, density P:159 / S:314-322).  KITTI outlier rule */
+/* (SPEC E-1, an external convention the paper invokes at P:131):       */
+/* outlier iff err > tau_abs (3 px) and err > tau_rel (5%) x the        */
+/* ground-truth magnitude.                                      */
+/* The decision is taken in float32 -- the kernel's precision, because  */
+/* a float decides an integer count -- with each operation rounded     */
+/* separately (no contraction).  Split 0 = all ground-truth pixels      */
+/* ("Occ"), split 1 = non-occluded ones ("Noc").  Over ground-truth     */
+/* pixels that the estimate covers ("Est"):                      */
+/*   D1 err = |d0 - gt_d0|,  D2 err = |d1 - gt_d1| (gt_d1 = disparity   */
+/*   at t+1 of the point seen at x), Fl err = |(u,v) - gt_flow|,         */
+/*   SF = D1 or D2 or Fl outlier.                                       */
+/* counts[s][0..5] = {n_gt, n_eval, n_d1, n_d2, n_fl, n_sf};            */
+/* density = n_eval / n_gt.  gt_valid may be NULL (every pixel).        */
+/* ------------------------------------------------------------------ */
+static int kitti_outlier(float err, float mag, float tau_abs, float tau_rel)
+{
+    const float rel = tau_rel * mag;
+    return err > tau_abs && err > rel;
+}
+
+int orc_evaluate(const float *sf, const uint8_t *valid_sf, const float *gt_d0,
+                 const float *gt_d1, const float *gt_flow, const uint8_t *gt_valid,
+                 const uint8_t *gt_noc, int W, int H, float tau_abs, float tau_rel,
+                 long long *counts /* [2][6] */)
+{
+    if (W < 1 || H < 1) return 1;
+    for (int k = 0; k < 12; ++k) counts[k] = 0;
+    for (int64_t p = 0; p < (int64_t)W * H; ++p) {
+        if (gt_valid && !gt_valid[p]) continue;
+        for (int split = 0; split < 2; ++split) {
+            if (split == 1 && !gt_noc[p]) continue;
+            long long *c = counts + 6 * split;
+            c[0] += 1;
+            if (!valid_sf[p]) continue;
+            c[1] += 1;
+            const float u = sf[4 * p + 0], v = sf[4 * p + 1];
+            const float d0 = sf[4 * p + 2], d1 = sf[4 * p + 3];
+            const float e1 = fabsf(d0 - gt_d0[p]);
+            const float e2 = fabsf(d1 - gt_d1[p]);
+            const float du = u - gt_flow[2 * p + 0], dv = v - gt_flow[2 * p + 1];
+            const float du2 = du * du, dv2 = dv * dv;
+            const float ef = sqrtf(du2 + dv2);
+            const float gu2 = gt_flow[2 * p + 0] * gt_flow[2 * p + 0];
+            const float gv2 = gt_flow[2 * p + 1] * gt_flow[2 * p + 1];
+            const float mf = sqrtf(gu2 + gv2);
+            const int o1 = kitti_outlier(e1, fabsf(gt_d0[p]), tau_abs, tau_rel);
+            const int o2 = kitti_outlier(e2, fabsf(gt_d1[p]), tau_abs, tau_rel);
+            const int of = kitti_outlier(ef, mf, tau_abs, tau_rel);
+            c[2] += o1;
+            c[3] += o2;
+            c[4] += of;
+            c[5] += (o1 || o2 || of);
+        }
+    }
+    return 0;
+}

@@ -243,16 +243,26 @@ def make_quad(cfg: Config | str, index: int = 0) -> dict:
             layers.append(_Layer(rect, dk, None, _texture(rng, th, tw, max(cfg.n_edges // 8, 1)),
                                  margin, t, zoom, zoom, 0.0, centre))
     il0, ir0, gt_d0, lid0 = _render(layers, W, H, 0)
-    il1, ir1, gt_d1, _ = _render(layers, W, H, 1)
+    il1, ir1, gt_d1, lid1 = _render(layers, W, H, 1)
     ys, xs = np.mgrid[0:H, 0:W].astype(np.float64)
     flow = np.zeros((H, W, 2), np.float64)
+    gt_d1w = np.zeros((H, W), np.float64)
     for k, L in enumerate(layers):
         m = lid0 == k
         qx, qy = L.from_t(xs[m], ys[m], 1)
         flow[m, 0] = qx - xs[m]
         flow[m, 1] = qy - ys[m]
+        gt_d1w[m] = L.disp(ys[m], 1)            # disparity at t+1 of the point seen at x
+    # non-occluded: the point seen at x at t lands inside the image at t+1 and is the
+    # visible layer there (KITTI "noc" semantics, P:131 / Table 1 caption)
+    qx = np.floor(xs + flow[..., 0] + 0.5).astype(np.int64)
+    qy = np.floor(ys + flow[..., 1] + 0.5).astype(np.int64)
+    inside = (qx >= 0) & (qx < W) & (qy >= 0) & (qy < H)
+    noc = np.zeros((H, W), bool)
+    noc[inside] = lid1[qy[inside], qx[inside]] == lid0[inside]
     return {"il0": il0, "ir0": ir0, "il1": il1, "ir1": ir1,
             "flow": flow.astype(np.float32), "gt_d0": gt_d0, "gt_d1": gt_d1,
+            "gt_d1w": gt_d1w.astype(np.float32), "gt_noc": noc.astype(np.uint8),
             "config": cfg.name, "seed": seed}
 
 
@@ -301,3 +311,24 @@ def random_flow(W, H, seed, scale=8.0, integer=False):
     if integer:
         f = np.round(f)
     return f.astype(np.float32)
+
+
+def random_eval_instance(H, W, seed, n=None):
+    """Seeded estimate + ground truth for the evaluation step ("random
+    instances"): GT disparities in [0, 80), GT flow ~ N(0, 15); the estimate is the GT
+    plus a per-channel error drawn from {0, N(0,1), N(0,4), N(0,30)} (40/30/20/10 %),
+    so every outlier decision is exercised; ~80 % est-valid, ~90 % GT-valid, ~85 % of
+    those non-occluded.  Leading batch axis ``n`` if given."""
+    rng = np.random.default_rng(seed)
+    shp = (H, W) if n is None else (n, H, W)
+    gd0 = rng.uniform(0, 80, shp).astype(np.float32)
+    gd1 = rng.uniform(0, 80, shp).astype(np.float32)
+    gfl = rng.normal(0, 15, shp + (2,)).astype(np.float32)
+    scale = rng.choice([0.0, 1.0, 4.0, 30.0], size=shp + (4,), p=[0.4, 0.3, 0.2, 0.1])
+    sf = np.stack([gfl[..., 0], gfl[..., 1], gd0, gd1], -1) + \
+        (scale * rng.normal(0, 1, shp + (4,))).astype(np.float32)
+    v = (rng.random(shp) < 0.8).astype(np.uint8)
+    gv = (rng.random(shp) < 0.9).astype(np.uint8)
+    noc = ((rng.random(shp) < 0.85) & (gv > 0)).astype(np.uint8)
+    return {"sf": sf.astype(np.float32), "valid_sf": v, "gt_d0": gd0, "gt_d1": gd1,
+            "gt_flow": gfl, "gt_noc": noc, "gt_valid": gv}
