@@ -200,6 +200,31 @@ SGM_API sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *
                                const sgm_camera *cam, const sgm_sceneflow_out *out,
                                void *stream);
 
+/* ---- evaluation ---------------------------------- */
+/* KITTI scene-flow outlier counts for n quadruples (Table 1 semantics P:130-155,
+ * "Est" = sparse evaluation; density P:159; outlier rule SPEC E-1 / S:467, an
+ * external convention the paper invokes as "the KITTI metric").  Over the
+ * ground-truth pixels (gt_valid != 0; NULL = every pixel) that the estimate covers
+ * (valid_sf != 0), a pixel is a D1 / D2 / Fl outlier iff its error exceeds tau_abs
+ * AND tau_rel x the ground-truth magnitude:  D1 |d0 - gt_d0|, D2 |d1 - gt_d1|,
+ * Fl ||(u,v) - gt_flow|| against ||gt_flow||, each decided in float32 with
+ * separately rounded operations; SF = outlier in any of the three.  Split 0 = all
+ * ground-truth pixels ("Occ"), split 1 = those with gt_noc != 0 ("Noc").
+ *   sf [n][H][W][4], valid_sf [n][H][W]  (sgm_scene_flow's outputs);
+ *   gt_d0, gt_d1 [n][H][W] float32 (gt_d1 = disparity at t+1 of the point seen
+ *   at x, i.e. already warped to frame t); gt_flow [n][H][W][2] float32;
+ *   gt_valid (nullable), gt_noc [n][H][W] uint8.  All device memory, sf 16-byte and
+ *   gt_flow 8-byte aligned.
+ *   counts: device [n][2][6] uint64 = {n_gt, n_eval, n_d1, n_d2, n_fl, n_sf} per
+ *   split; overwritten (zeroed on `stream`, then integer atomics: deterministic).
+ *   Rates = n_x / n_eval, density = n_eval / n_gt.
+ * SGM_ERR_INVALID_ARGUMENT on NULL required pointers, misalignment, n outside
+ * 1..max_batch, tau_abs < 0 or tau_rel < 0 (or NaN).  One kernel launch. */
+SGM_API sgm_status sgm_evaluate(sgm_handle *h, int32_t n, const float *sf, const uint8_t *valid_sf,
+                        const float *gt_d0, const float *gt_d1, const float *gt_flow,
+                        const uint8_t *gt_valid, const uint8_t *gt_noc, float tau_abs,
+                        float tau_rel, uint64_t *counts, void *stream);
+
 /* ---- instrumentation ----------------------------------------------------- */
 enum { SGM_NUM_STAGES = 5 };   /* census, sweep_fwd, sweep_bwd_wta, lr_check, combine */
 

@@ -25,6 +25,7 @@ EXPORTS = (
     "sgm_wta", "sgm_lr_check", "sgm_disparity", "sgm_combine_sceneflow", "sgm_scene_flow",
     "sgm_scene_flow_host", "sgm_set_timing", "sgm_read_timing", "sgm_stage_name",
     "sgm_launch_count", "sgm_get_geometry", "sgm_last_error_string", "sgm_debug_set_trace",
+    "sgm_evaluate",
 )
 
 
@@ -105,6 +106,7 @@ def load(path: str | None = None):
                                 ctypes.POINTER(SgmSceneflowOut), P]),
         "sgm_scene_flow_host": (st, [P, I32, P, P, P, ctypes.POINTER(SgmCamera),
                                      ctypes.POINTER(SgmSceneflowOut), P]),
+        "sgm_evaluate": (st, [P, I32, P, P, P, P, P, P, P, ctypes.c_float, ctypes.c_float, P, P]),
         "sgm_set_timing": (st, [P, I32]),
         "sgm_read_timing": (I32, [P, ctypes.POINTER(ctypes.c_float)]),
         "sgm_stage_name": (ctypes.c_char_p, [I32]),

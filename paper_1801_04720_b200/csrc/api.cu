@@ -388,6 +388,28 @@ sgm_status sgm_combine_sceneflow(sgm_handle *h, const float *d0, const uint8_t *
     return from_cuda(e);
 }
 
+sgm_status sgm_evaluate(sgm_handle *h, int32_t n, const float *sf, const uint8_t *valid_sf,
+                        const float *gt_d0, const float *gt_d1, const float *gt_flow,
+                        const uint8_t *gt_valid, const uint8_t *gt_noc, float tau_abs,
+                        float tau_rel, uint64_t *counts, void *stream) {
+    if (!h || !sf || !valid_sf || !gt_d0 || !gt_d1 || !gt_flow || !gt_noc || !counts)
+        return SGM_ERR_INVALID_ARGUMENT;
+    if (n < 1 || n > h->prm.max_batch) return SGM_ERR_INVALID_ARGUMENT;
+    if (!(tau_abs >= 0.f) || !(tau_rel >= 0.f)) return SGM_ERR_INVALID_ARGUMENT;
+    if (!aligned16(sf) || (reinterpret_cast<uintptr_t>(gt_flow) & 7) ||
+        (reinterpret_cast<uintptr_t>(gt_d0) & 3) || (reinterpret_cast<uintptr_t>(gt_d1) & 3) ||
+        (reinterpret_cast<uintptr_t>(counts) & 7))
+        return SGM_ERR_INVALID_ARGUMENT;
+    sgm::EvalParams p{};
+    p.W = h->prm.width; p.H = h->prm.height; p.nquads = n;
+    p.sf = sf; p.valid_sf = valid_sf; p.gt_d0 = gt_d0; p.gt_d1 = gt_d1; p.gt_flow = gt_flow;
+    p.gt_valid = gt_valid; p.gt_noc = gt_noc; p.tau_abs = tau_abs; p.tau_rel = tau_rel;
+    p.counts = counts;
+    cudaError_t e = sgm::launch_evaluate(p, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) ++h->launches;
+    return from_cuda(e);
+}
+
 static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *images, int64_t pitch,
                                   const float *flow, const uint8_t *flow_valid,
                                   const sgm_camera *cam, const sgm_sceneflow_out *out,

@@ -70,6 +70,14 @@ struct CombineParams {
     float *sf, *p0, *dp; uint8_t *valid_sf, *valid_3d;
 };
 
+struct EvalParams {
+    int W, H, nquads;
+    const float *sf; const uint8_t *valid_sf;
+    const float *gt_d0, *gt_d1, *gt_flow; const uint8_t *gt_valid, *gt_noc;
+    float tau_abs, tau_rel;
+    uint64_t *counts;                      // [nquads][2][6]
+};
+
 // ----------------------------------------------------------------- launchers (host)
 cudaError_t launch_census(const uint8_t *const *imgs, int nimg, long long pitch, int W, int H,
                           int cw, int ch, uint64_t *out, long long out_stride, cudaStream_t st);
@@ -84,5 +92,6 @@ cudaError_t launch_lr(const LrParams &p, cudaStream_t st);
 cudaError_t launch_repitch(const uint8_t *src, uint8_t *dst, int W, long long pitch, long long rows,
                            cudaStream_t st);
 cudaError_t launch_combine(const CombineParams &p, cudaStream_t st);
+cudaError_t launch_evaluate(const EvalParams &p, cudaStream_t st);
 
 }  // namespace sgm

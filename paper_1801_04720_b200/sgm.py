@@ -206,6 +206,33 @@ class SGM:
                   ctypes.byref(camera.c()), ctypes.byref(o), _stream(stream))
         return out
 
+    def evaluate(self, sf, valid_sf, gt_d0, gt_d1, gt_flow, gt_noc, gt_valid=None,
+                 tau_abs=3.0, tau_rel=0.05, counts=None, stream=None):
+        """KITTI outlier counts (sgm_evaluate): device tensors sf [n][H][W][4],
+        valid_sf/gt_noc/gt_valid uint8 [n][H][W], gt_d0/gt_d1 float32 [n][H][W],
+        gt_flow float32 [n][H][W][2].  Returns int64 counts [n][2][6] (device)."""
+        n = int(sf.shape[0])
+        if counts is None:
+            counts = torch.empty((n, 2, 6), dtype=torch.int64, device=sf.device)
+        _lib.call("sgm_evaluate", self.h, n, _ptr(sf), _ptr(valid_sf), _ptr(gt_d0), _ptr(gt_d1),
+                  _ptr(gt_flow), _ptr(gt_valid), _ptr(gt_noc), float(tau_abs), float(tau_rel),
+                  _ptr(counts), _stream(stream))
+        return counts
+
+
+def rates_from_counts(counts):
+    """{split: {D1, D2, Fl, SF (percent of evaluated pixels), density (percent)}} from
+    one [2][6] count block (host arithmetic on integers the kernel produced)."""
+    c = [[int(v) for v in row] for row in counts]
+    out = {}
+    for split, name in ((0, "occ"), (1, "noc")):
+        n_gt, n_ev = c[split][0], c[split][1]
+        r = {k: (100.0 * c[split][i] / n_ev if n_ev else float("nan"))
+             for k, i in (("D1", 2), ("D2", 3), ("Fl", 4), ("SF", 5))}
+        r["density"] = 100.0 * n_ev / n_gt if n_gt else float("nan")
+        out[name] = r
+    return out
+
 
 def stack_quads(quads, pitch, device):
     """Host quads (synth.make_quad dicts) -> device images [n][4][H][pitch], flow [n][H][W][2]."""

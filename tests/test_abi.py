@@ -70,6 +70,8 @@ def test_null_handle_calls_are_rejected():
     lib = _lib.load()
     assert lib.sgm_census(None, None, 64, None, None) == 1
     assert lib.sgm_scene_flow(None, 1, None, 64, None, None, None, None, None) == 1
+    assert lib.sgm_evaluate(None, 1, None, None, None, None, None, None, None, 3.0, 0.05,
+                            None, None) == 1
     assert lib.sgm_launch_count(None) == 0
     lib.sgm_destroy(None)
 
