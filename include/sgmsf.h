@@ -216,10 +216,12 @@ SGM_API sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *
  *   gt_valid (nullable), gt_noc [n][H][W] uint8.  All device memory, sf 16-byte and
  *   gt_flow 8-byte aligned.
  *   counts: device [n][2][6] uint64 = {n_gt, n_eval, n_d1, n_d2, n_fl, n_sf} per
- *   split; overwritten (zeroed on `stream`, then integer atomics: deterministic).
+ *   split; overwritten (integer sums in a fixed order: deterministic).  Uses
+ *   per-handle scratch: do not run two sgm_evaluate calls of one handle concurrently.
  *   Rates = n_x / n_eval, density = n_eval / n_gt.
  * SGM_ERR_INVALID_ARGUMENT on NULL required pointers, misalignment, n outside
- * 1..max_batch, tau_abs < 0 or tau_rel < 0 (or NaN).  One kernel launch. */
+ * 1..max_batch, tau_abs < 0 or tau_rel < 0 (or NaN), counts not 8-byte aligned.
+ * One kernel launch. */
 SGM_API sgm_status sgm_evaluate(sgm_handle *h, int32_t n, const float *sf, const uint8_t *valid_sf,
                         const float *gt_d0, const float *gt_d1, const float *gt_flow,
                         const uint8_t *gt_valid, const uint8_t *gt_noc, float tau_abs,

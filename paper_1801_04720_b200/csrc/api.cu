@@ -33,6 +33,7 @@ struct sgm_handle {
     uint8_t *lr_valid = nullptr;
     uint16_t *gbuf = nullptr;       // [4*max_batch][nbands][W][3][Dp]
     int *sync = nullptr;            // [1 + 4*max_batch*nbands]
+    unsigned *eval_part = nullptr;  // [evaluate_max_blocks() + max_batch][12] + ticket
     // staging for the _host entry point (device): two slots so that back-to-back calls
     // pipeline (upload of call k+1 and download of call k-1 overlap the kernels of call k)
     long long stage_pitch = 0;
@@ -77,7 +78,7 @@ cudaError_t dalloc(T **p, size_t count) {
 
 void free_all(sgm_handle *h) {
     void *ptrs[] = {h->census, h->sfwd, h->dint, h->dsub, h->lr_int, h->lr_sub, h->lr_valid,
-                    h->gbuf, h->sync, h->sync_host};
+                    h->gbuf, h->sync, h->sync_host, h->eval_part};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (auto &st : h->stage) {
@@ -182,6 +183,9 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     if (e == cudaSuccess) e = dalloc(&h->gbuf, nv * size_t(h->nbands) * size_t(W) * 3 * size_t(h->dp));
     if (e == cudaSuccess) e = dalloc(&h->sync, 1 + nv * size_t(h->nbands));
     if (e == cudaSuccess) e = dalloc(&h->sync_host, 1 + nv * size_t(h->nbands));
+    const size_t eval_rows = size_t(sgm::evaluate_max_blocks()) + size_t(p->max_batch);
+    if (e == cudaSuccess) e = dalloc(&h->eval_part, eval_rows * 12 + 1);
+    if (e == cudaSuccess) e = cudaMemset(h->eval_part + eval_rows * 12, 0, sizeof(unsigned));
     const size_t mb = size_t(p->max_batch);
     for (auto &st : h->stage) {
         if (e == cudaSuccess) e = dalloc(&st.img_dense, nv * size_t(H) * size_t(W));
@@ -404,7 +408,9 @@ sgm_status sgm_evaluate(sgm_handle *h, int32_t n, const float *sf, const uint8_t
     p.W = h->prm.width; p.H = h->prm.height; p.nquads = n;
     p.sf = sf; p.valid_sf = valid_sf; p.gt_d0 = gt_d0; p.gt_d1 = gt_d1; p.gt_flow = gt_flow;
     p.gt_valid = gt_valid; p.gt_noc = gt_noc; p.tau_abs = tau_abs; p.tau_rel = tau_rel;
-    p.counts = counts;
+    p.counts = reinterpret_cast<unsigned long long *>(counts);
+    p.part = h->eval_part;
+    p.ticket = h->eval_part + (size_t(sgm::evaluate_max_blocks()) + size_t(h->prm.max_batch)) * 12;
     cudaError_t e = sgm::launch_evaluate(p, static_cast<cudaStream_t>(stream));
     if (e == cudaSuccess) ++h->launches;
     return from_cuda(e);

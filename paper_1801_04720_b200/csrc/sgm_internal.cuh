@@ -75,7 +75,9 @@ struct EvalParams {
     const float *sf; const uint8_t *valid_sf;
     const float *gt_d0, *gt_d1, *gt_flow; const uint8_t *gt_valid, *gt_noc;
     float tau_abs, tau_rel;
-    uint64_t *counts;                      // [nquads][2][6]
+    unsigned long long *counts;            // [nquads][2][6]
+    unsigned *part;                        // [grid blocks][12] block partials (scratch)
+    unsigned *ticket;                      // zero between launches (the last block resets it)
 };
 
 // ----------------------------------------------------------------- launchers (host)
@@ -93,5 +95,6 @@ cudaError_t launch_repitch(const uint8_t *src, uint8_t *dst, int W, long long pi
                            cudaStream_t st);
 cudaError_t launch_combine(const CombineParams &p, cudaStream_t st);
 cudaError_t launch_evaluate(const EvalParams &p, cudaStream_t st);
+int evaluate_max_blocks();   // scratch rows launch_evaluate may use besides one per quad
 
 }  // namespace sgm

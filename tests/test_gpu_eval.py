@@ -64,6 +64,30 @@ def test_evaluate_parity(orc, dev, shape, with_gv):
     g.close()
 
 
+def test_evaluate_misaligned_inputs(orc, dev):
+    """Byte masks and GT maps that do not start on a 16-byte boundary take the scalar
+    kernel; the counts are the same."""
+    W, H, n = 61, 13, 3
+    inst = synth.random_eval_instance(H, W, seed=99, n=n)
+    g = _handle(W, H, n)
+    t = _dev(inst, dev)
+
+    def shifted(x):
+        flat = x.reshape(-1)
+        buf = torch.empty(flat.numel() + 1, dtype=x.dtype, device=dev)
+        buf[1:] = flat
+        return buf[1:].view(x.shape)
+
+    for key in ("valid_sf", "gt_noc", "gt_valid", "gt_d0"):
+        tt = dict(t)
+        tt[key] = shifted(t[key])
+        assert tt[key].data_ptr() % 16 != 0
+        c = _gpu_counts(g, tt)
+        for i in range(n):
+            assert np.array_equal(c[i], _orc_counts(orc, inst, i)), key
+    g.close()
+
+
 def test_evaluate_thresholds(orc, dev):
     W, H, n = 64, 20, 2
     inst = synth.random_eval_instance(H, W, seed=7, n=n)
