@@ -8,5 +8,5 @@ this module only builds it and marshals numpy arrays through ctypes.
 """
 from .oracle import (  # noqa: F401
     build, census, cost, path, aggregate, wta, lr_check, sgm_view, disparity,
-    combine, reproject, evaluate, run_quad, lib_path,
+    combine, reproject, evaluate, run_quad, run_stream, lib_path,
 )

@@ -237,3 +237,38 @@ def run_quad(quad, prm, rule=0, threads=True):
     p0, p1, dp, v3 = reproject(sf, vsf, prm["f"], prm["B"], cx, cy)
     return {"disp0": res["t0"], "disp1": res["t1"], "sf": sf, "valid_sf": vsf,
             "p0": p0, "p1": p1, "dp": dp, "valid_3d": v3}
+
+
+def run_stream(video, prm, rule=0, threads=True):
+    """Streaming mode ("reuse"): a stereo video of n+1 frames
+    gives n quads (frame k, frame k+1).  Every frame's LR-checked map is computed once and
+    serves as D1 of quad k-1 and D0 of quad k; the combination and 3D are those of
+    run_quad.  ``video`` holds left, right uint8 [n+1][H][W] and flow [n][H][W][2]."""
+    left, right, flow = video["left"], video["right"], video["flow"]
+    n = flow.shape[0]
+    args = (prm["D"], prm["cw"], prm["ch"], prm["P1"], prm["P2"], prm["T"])
+    maps = [None] * (n + 1)
+
+    def run(k):
+        maps[k] = disparity(left[k], right[k], *args)
+
+    if threads:
+        th = [threading.Thread(target=run, args=(k,)) for k in range(n + 1)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    else:
+        for k in range(n + 1):
+            run(k)
+    H, W = left.shape[1:]
+    cx = prm.get("cx", (W - 1) / 2.0)
+    cy = prm.get("cy", (H - 1) / 2.0)
+    quads = []
+    for k in range(n):
+        sf, vsf = combine(maps[k]["d_sub"], maps[k]["valid"], maps[k + 1]["d_sub"],
+                          maps[k + 1]["valid"], flow[k], None, rule)
+        p0, p1, dp, v3 = reproject(sf, vsf, prm["f"], prm["B"], cx, cy)
+        quads.append({"disp0": maps[k], "disp1": maps[k + 1], "sf": sf, "valid_sf": vsf,
+                      "p0": p0, "p1": p1, "dp": dp, "valid_3d": v3})
+    return {"maps": maps, "quads": quads}

@@ -139,19 +139,23 @@ class _Layer:
         self.dadd = dadd                              # disparity offset at t+1
         self.c = np.asarray(centre, np.float64)
 
-    # frame-t layer point p  <->  frame-f image point q (left view)
+    # frame-t layer point p  <->  image point q of a frame with motion amount u (left
+    # view): q = c + zoom^u (p - c) + u * shift.  u = 0 is frame t, u = 1 frame t+1 of a
+    # quad; videos (make_video) visit u = 0, 1, 2, 1, 0, ...
     def to_t(self, qx, qy, frame):
         if frame == 0:
             return qx, qy
-        px = self.c[0] + (qx - self.c[0] - self.shift[0]) / self.zoom
-        py = self.c[1] + (qy - self.c[1] - self.shift[1]) / self.zoom
+        s = self.zoom ** frame
+        px = self.c[0] + (qx - self.c[0] - self.shift[0] * frame) / s
+        py = self.c[1] + (qy - self.c[1] - self.shift[1] * frame) / s
         return px, py
 
     def from_t(self, px, py, frame):
         if frame == 0:
             return px, py
-        return (self.c[0] + self.zoom * (px - self.c[0]) + self.shift[0],
-                self.c[1] + self.zoom * (py - self.c[1]) + self.shift[1])
+        s = self.zoom ** frame
+        return (self.c[0] + s * (px - self.c[0]) + self.shift[0] * frame,
+                self.c[1] + s * (py - self.c[1]) + self.shift[1] * frame)
 
     def covers(self, px, py):
         if self.rect is None:
@@ -166,7 +170,7 @@ class _Layer:
 
     def disp(self, py, frame):
         d = self.disp_t(py)
-        return d if frame == 0 else d * self.dscale + self.dadd
+        return d if frame == 0 else d * self.dscale ** frame + self.dadd * frame
 
 
 def _render(layers, W, H, frame):
@@ -206,7 +210,17 @@ def make_quad(cfg: Config | str, index: int = 0) -> dict:
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
     seed = cfg.seed + index
-    rng = np.random.default_rng(seed)
+    W, H = cfg.W, cfg.H
+    layers = _build_layers(cfg, np.random.default_rng(seed))
+    il0, ir0, gt_d0, lid0 = _render(layers, W, H, 0)
+    il1, ir1, gt_d1, lid1 = _render(layers, W, H, 1)
+    flow, gt_d1w, noc = _motion(layers, W, H, 0, 1, lid0, lid1)
+    return {"il0": il0, "ir0": ir0, "il1": il1, "ir1": ir1,
+            "flow": flow, "gt_d0": gt_d0, "gt_d1": gt_d1, "gt_d1w": gt_d1w, "gt_noc": noc,
+            "config": cfg.name, "seed": seed}
+
+
+def _build_layers(cfg: Config, rng) -> list:
     W, H = cfg.W, cfg.H
     centre = ((W - 1) / 2.0, (H - 1) / 2.0)
     dmax = cfg.D + 8
@@ -242,28 +256,67 @@ def make_quad(cfg: Config | str, index: int = 0) -> dict:
         for dk, rect, t in boxes:
             layers.append(_Layer(rect, dk, None, _texture(rng, th, tw, max(cfg.n_edges // 8, 1)),
                                  margin, t, zoom, zoom, 0.0, centre))
-    il0, ir0, gt_d0, lid0 = _render(layers, W, H, 0)
-    il1, ir1, gt_d1, lid1 = _render(layers, W, H, 1)
+    return layers
+
+
+def _motion(layers, W, H, ua, ub, lid_a, lid_b):
+    """Flow from the frame with motion amount ua to the one with ub, the disparity at ub
+    of the point seen at each pixel of ua, and the non-occluded mask."""
     ys, xs = np.mgrid[0:H, 0:W].astype(np.float64)
     flow = np.zeros((H, W, 2), np.float64)
     gt_d1w = np.zeros((H, W), np.float64)
     for k, L in enumerate(layers):
-        m = lid0 == k
-        qx, qy = L.from_t(xs[m], ys[m], 1)
+        m = lid_a == k
+        px, py = L.to_t(xs[m], ys[m], ua)       # layer point seen at x in frame ua
+        qx, qy = L.from_t(px, py, ub)
         flow[m, 0] = qx - xs[m]
         flow[m, 1] = qy - ys[m]
-        gt_d1w[m] = L.disp(ys[m], 1)            # disparity at t+1 of the point seen at x
-    # non-occluded: the point seen at x at t lands inside the image at t+1 and is the
+        gt_d1w[m] = L.disp(py, ub)              # disparity at ub of the point seen at x
+    # non-occluded: the point seen at x lands inside the image in frame ub and is the
     # visible layer there (KITTI "noc" semantics, P:131 / Table 1 caption)
     qx = np.floor(xs + flow[..., 0] + 0.5).astype(np.int64)
     qy = np.floor(ys + flow[..., 1] + 0.5).astype(np.int64)
     inside = (qx >= 0) & (qx < W) & (qy >= 0) & (qy < H)
     noc = np.zeros((H, W), bool)
-    noc[inside] = lid1[qy[inside], qx[inside]] == lid0[inside]
-    return {"il0": il0, "ir0": ir0, "il1": il1, "ir1": ir1,
-            "flow": flow.astype(np.float32), "gt_d0": gt_d0, "gt_d1": gt_d1,
-            "gt_d1w": gt_d1w.astype(np.float32), "gt_noc": noc.astype(np.uint8),
-            "config": cfg.name, "seed": seed}
+    noc[inside] = lid_b[qy[inside], qx[inside]] == lid_a[inside]
+    return flow.astype(np.float32), gt_d1w.astype(np.float32), noc.astype(np.uint8)
+
+
+# motion amount of video frame k (bounded, so disparities stay inside [0, D-1])
+VIDEO_MOTION = (0, 1, 2, 1)
+
+
+def make_video(cfg: Config | str, n_quads: int, index: int = 0) -> dict:
+    """A seeded stereo video of n_quads + 1 frames for the streaming mode (SURVEY 8(f)
+    rank 3): the scene of make_quad(cfg, index), with motion amount
+    VIDEO_MOTION[k % 4] at frame k, so frames 0 and 1 are exactly that quad's.
+    left, right uint8 [n+1][H][W]; flow float32 [n][H][W][2] (frame k -> k+1); gt_d
+    float32 [n+1][H][W]; gt_d1w float32 [n][H][W] (disparity at k+1 of the point seen at
+    x in frame k); gt_noc uint8 [n][H][W]."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    seed = cfg.seed + index
+    W, H = cfg.W, cfg.H
+    layers = _build_layers(cfg, np.random.default_rng(seed))
+    us = [VIDEO_MOTION[k % len(VIDEO_MOTION)] for k in range(n_quads + 1)]
+    frames = [_render(layers, W, H, u) for u in us]
+    out = {"left": np.stack([f[0] for f in frames]), "right": np.stack([f[1] for f in frames]),
+           "gt_d": np.stack([f[2] for f in frames]), "config": cfg.name, "seed": seed,
+           "motion": us}
+    flows, d1w, nocs = [], [], []
+    for k in range(n_quads):
+        f, d, m = _motion(layers, W, H, us[k], us[k + 1], frames[k][3], frames[k + 1][3])
+        flows.append(f); d1w.append(d); nocs.append(m)
+    out.update(flow=np.stack(flows), gt_d1w=np.stack(d1w), gt_noc=np.stack(nocs))
+    return out
+
+
+def video_quad(video: dict, k: int) -> dict:
+    """Quad k of a video as a make_quad-style dict (frames k and k+1)."""
+    return {"il0": video["left"][k], "ir0": video["right"][k], "il1": video["left"][k + 1],
+            "ir1": video["right"][k + 1], "flow": video["flow"][k],
+            "gt_d0": video["gt_d"][k], "gt_d1": video["gt_d"][k + 1],
+            "gt_d1w": video["gt_d1w"][k], "gt_noc": video["gt_noc"][k]}
 
 
 def make_batch(cfg: Config | str, start: int, count: int) -> list:

@@ -424,3 +424,35 @@ def test_lr_row_hand_example(orc):
     assert list(v[0]) == ex["valid"]
     assert list(oi[0]) == [d if ok else -1 for d, ok in zip(ex["dl"], ex["valid"])]
     assert list(os_[0]) == [d + 0.25 if ok else -1.0 for d, ok in zip(ex["dl"], ex["valid"])]
+
+
+def test_stream_equals_independent_quads(orc):
+    """Streaming mode: reusing frame k's map as D1 of quad
+    k-1 and D0 of quad k changes nothing -- every quad is bit-identical to run_quad on
+    (frame k, frame k+1)."""
+    cfg = synth.CONFIGS["tiny"]
+    prm = synth.sgm_params(cfg)
+    v = synth.make_video(cfg, 4, 0)
+    s = orc.run_stream(v, prm)
+    assert len(s["maps"]) == 5 and len(s["quads"]) == 4
+    for k in range(4):
+        r = orc.run_quad(synth.video_quad(v, k), prm)
+        for key in ("sf", "valid_sf", "p0", "dp", "valid_3d"):
+            assert np.array_equal(s["quads"][k][key], r[key]), (k, key)
+        for key in ("d_sub", "valid", "d_int"):
+            assert np.array_equal(s["quads"][k]["disp0"][key], r["disp0"][key])
+            assert np.array_equal(s["quads"][k]["disp1"][key], r["disp1"][key])
+
+
+def test_video_generator_frames_match_quads():
+    """make_video's frames 0/1 are make_quad's; later frames follow VIDEO_MOTION."""
+    q = synth.make_quad("tiny", 2)
+    v = synth.make_video("tiny", 3, 2)
+    q0 = synth.video_quad(v, 0)
+    for key in ("il0", "ir0", "il1", "ir1", "flow", "gt_d0", "gt_d1", "gt_d1w", "gt_noc"):
+        assert np.array_equal(q[key], q0[key]), key
+    # frame 3 has the motion amount of frame 1 (0, 1, 2, 1): identical images
+    assert v["motion"] == [0, 1, 2, 1]
+    assert np.array_equal(v["left"][1], v["left"][3]) and np.array_equal(v["right"][1], v["right"][3])
+    # flows k -> k+1 and back cancel on the tiny pure translation
+    assert np.allclose(v["flow"][1], -v["flow"][2])
