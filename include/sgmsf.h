@@ -200,6 +200,30 @@ SGM_API sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *
                                const sgm_camera *cam, const sgm_sceneflow_out *out,
                                void *stream);
 
+/* ---- streaming (video) mode ---------------------- */
+/* n consecutive scene-flow quads of ONE stereo video share their frames: quad k =
+ * (frame k, frame k+1), so each frame's LR-checked disparity map is computed once and
+ * serves as D1 of quad k-1 and D0 of quad k -- n+1 SGM pairs instead of 2n (the reuse
+ * the paper names as future work).  Every quad's results are bit-identical to
+ * sgm_scene_flow on (frame k, frame k+1).
+ *   images: [n+1][2][H] rows of pitch_bytes, frame k = (I_l^k, I_r^k) (pitch % 16 == 0,
+ *   16-byte aligned); flow: [n][H][W][2] from frame k to k+1; flow_valid [n][H][W] or
+ *   NULL; out->sf, valid_sf, p0, dp, valid_3d: per quad, [n][...] as in sgm_scene_flow;
+ *   out->disp_int / disp_sub / disp_valid (optional): per FRAME, [n+1][H][W].
+ * 1 <= n <= max_batch.  5 kernel launches for the whole video segment. */
+SGM_API sgm_status sgm_scene_flow_stream(sgm_handle *h, int32_t n, const uint8_t *images,
+                                 int64_t pitch_bytes, const float *flow,
+                                 const uint8_t *flow_valid, const sgm_camera *cam,
+                                 const sgm_sceneflow_out *out, void *stream);
+
+/* Host-buffer twin of sgm_scene_flow_stream, pipelined exactly like
+ * sgm_scene_flow_host: images dense [n+1][2][H][W] pinned host memory, the other
+ * buffers host memory with the shapes above. */
+SGM_API sgm_status sgm_scene_flow_stream_host(sgm_handle *h, int32_t n, const uint8_t *images,
+                                      const float *flow, const uint8_t *flow_valid,
+                                      const sgm_camera *cam, const sgm_sceneflow_out *out,
+                                      void *stream);
+
 /* ---- evaluation ---------------------------------- */
 /* KITTI scene-flow outlier counts for n quadruples (Table 1 semantics P:130-155,
  * "Est" = sparse evaluation; density P:159; outlier rule SPEC E-1 / S:467, an

@@ -5,7 +5,7 @@ csrc/*.cu; ``SGM`` is its thin torch-tensor binding.  Importing this package
 does not touch the GPU; creating an ``SGM`` loads the library and fails loudly
 if it is missing (there is no CPU fallback).
 """
-__all__ = ["SGM", "Camera", "stack_quads", "pitch_for", "rates_from_counts"]
+__all__ = ["SGM", "Camera", "stack_quads", "pitch_for", "rates_from_counts", "stack_video"]
 
 
 def __getattr__(name):

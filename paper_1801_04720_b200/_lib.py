@@ -25,7 +25,7 @@ EXPORTS = (
     "sgm_wta", "sgm_lr_check", "sgm_disparity", "sgm_combine_sceneflow", "sgm_scene_flow",
     "sgm_scene_flow_host", "sgm_set_timing", "sgm_read_timing", "sgm_stage_name",
     "sgm_launch_count", "sgm_get_geometry", "sgm_last_error_string", "sgm_debug_set_trace",
-    "sgm_evaluate",
+    "sgm_evaluate", "sgm_scene_flow_stream", "sgm_scene_flow_stream_host",
 )
 
 
@@ -104,7 +104,11 @@ def load(path: str | None = None):
                                        P, P, P]),
         "sgm_scene_flow": (st, [P, I32, P, I64, P, P, ctypes.POINTER(SgmCamera),
                                 ctypes.POINTER(SgmSceneflowOut), P]),
+        "sgm_scene_flow_stream": (st, [P, I32, P, I64, P, P, ctypes.POINTER(SgmCamera),
+                                ctypes.POINTER(SgmSceneflowOut), P]),
         "sgm_scene_flow_host": (st, [P, I32, P, P, P, ctypes.POINTER(SgmCamera),
+                                     ctypes.POINTER(SgmSceneflowOut), P]),
+        "sgm_scene_flow_stream_host": (st, [P, I32, P, P, P, ctypes.POINTER(SgmCamera),
                                      ctypes.POINTER(SgmSceneflowOut), P]),
         "sgm_evaluate": (st, [P, I32, P, P, P, P, P, P, P, ctypes.c_float, ctypes.c_float, P, P]),
         "sgm_set_timing": (st, [P, I32]),

@@ -95,9 +95,9 @@ void free_all(sgm_handle *h) {
         if (e) cudaEventDestroy(e);
 }
 
-sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int qoff = 0, int *sync = nullptr) {
+sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int *sync = nullptr) {
     sgm::SweepParams p{};
-    const long long v0 = 4LL * qoff;
+    const long long v0 = 0;
     p.W = h->prm.width; p.H = h->prm.height; p.D = h->prm.num_disp; p.Dp = h->dp;
     p.P1 = h->prm.p1; p.P2 = h->prm.p2; p.cmax = h->cmax;
     p.nviews = nviews; p.nbands = h->nbands;
@@ -416,12 +416,17 @@ sgm_status sgm_evaluate(sgm_handle *h, int32_t n, const float *sf, const uint8_t
     return from_cuda(e);
 }
 
-static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *images, int64_t pitch,
-                                  const float *flow, const uint8_t *flow_valid,
+// The batched hot path.  Quad mode: images [n][4][H][pitch] = n independent quads, 2n
+// stereo pairs, quad k combines pairs 2k and 2k+1.  Stream mode: images [n+1][2][H][pitch]
+// = n+1 frames of one stereo video, n+1 pairs, quad k combines pairs k and k+1 (each
+// frame's map computed once).  The disparity outputs are per pair.
+static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, bool stream, const uint8_t *images,
+                                  int64_t pitch, const float *flow, const uint8_t *flow_valid,
                                   const sgm_camera *cam, const sgm_sceneflow_out *out,
-                                  cudaStream_t st, int qoff = 0, int *sync = nullptr) {
+                                  cudaStream_t st, int *sync = nullptr) {
     const int W = h->prm.width, H = h->prm.height;
     const long long npx = h->npx;
+    const int npairs = stream ? n + 1 : 2 * n;
     const bool want3d = out->p0 || out->dp || out->valid_3d;
     if (want3d && (!out->dp || !out->valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
     if (want3d && !(cam->f_px > 0.f && cam->baseline_m > 0.f)) return SGM_ERR_INVALID_ARGUMENT;
@@ -430,15 +435,13 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *image
         if (timing) cudaEventRecord(h->ev[i], st);
     };
     mark(0);
-    cudaError_t e = sgm::launch_census_stack(images, (long long)H * pitch, 4 * n, pitch, W, H,
-                                             h->prm.census_w, h->prm.census_h,
-                                             h->census + 4LL * qoff * npx, npx, st);
+    cudaError_t e = sgm::launch_census_stack(images, (long long)H * pitch, 2 * npairs, pitch, W, H,
+                                             h->prm.census_w, h->prm.census_h, h->census, npx, st);
     if (e != cudaSuccess) return from_cuda(e);
     ++h->launches;
     mark(1);
-    const long long v0 = 4LL * qoff * npx;
     {
-        sgm::SweepParams p = sweep_params(h, 4 * n, qoff, sync);
+        sgm::SweepParams p = sweep_params(h, 2 * npairs, sync);
         int nl = 0;
         e = sgm::launch_sweeps(p, h->cpl, h->c64, h->nw, false, st, timing ? h->ev[2] : nullptr,
                                nullptr, &nl);
@@ -446,14 +449,14 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *image
         if (e != cudaSuccess) return from_cuda(e);
     }
     mark(3);
-    int16_t *di = out->disp_int ? out->disp_int : h->lr_int + 2LL * qoff * npx;
-    float *ds = out->disp_sub ? out->disp_sub : h->lr_sub + 2LL * qoff * npx;
-    uint8_t *dv = out->disp_valid ? out->disp_valid : h->lr_valid + 2LL * qoff * npx;
+    int16_t *di = out->disp_int ? out->disp_int : h->lr_int;
+    float *ds = out->disp_sub ? out->disp_sub : h->lr_sub;
+    uint8_t *dv = out->disp_valid ? out->disp_valid : h->lr_valid;
     {
         sgm::LrParams p{};
         p.W = W; p.H = H; p.T = h->prm.lr_threshold; p.invalid = h->prm.invalid_disp;
-        p.npairs = 2 * n;
-        p.dl = h->dint + v0; p.dls = h->dsub + v0; p.dr = h->dint + v0 + npx;
+        p.npairs = npairs;
+        p.dl = h->dint; p.dls = h->dsub; p.dr = h->dint + npx;
         p.in_stride_l = p.in_stride_r = 2 * npx;
         p.out_int = di; p.out_sub = ds; p.valid = dv; p.out_stride = npx;
         e = sgm::launch_lr(p, st);
@@ -464,7 +467,8 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *image
     {
         sgm::CombineParams p{};
         p.W = W; p.H = H; p.rule = h->prm.bilinear_rule; p.nquads = n;
-        p.d0 = ds; p.d1 = ds + npx; p.v0 = dv; p.v1 = dv + npx; p.disp_stride = 2 * npx;
+        p.d0 = ds; p.d1 = ds + npx; p.v0 = dv; p.v1 = dv + npx;
+        p.disp_stride = stream ? npx : 2 * npx;
         p.flow = flow; p.flow_valid = flow_valid;
         if (cam) {
             p.f = cam->f_px; p.B = cam->baseline_m; p.cx = cam->cx; p.cy = cam->cy;
@@ -481,24 +485,43 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, const uint8_t *image
     return SGM_OK;
 }
 
-sgm_status sgm_scene_flow(sgm_handle *h, int32_t n, const uint8_t *images, int64_t pitch_bytes,
-                          const float *flow, const uint8_t *flow_valid, const sgm_camera *cam,
-                          const sgm_sceneflow_out *out, void *stream) {
+// Both modes take 1..max_batch quads (stream mode: n+1 <= 2 max_batch pairs fit the
+// 4 max_batch views of scratch).
+static bool batch_ok(const sgm_handle *h, int32_t n, bool) { return n >= 1 && n <= h->prm.max_batch; }
+
+static sgm_status scene_flow_dev(sgm_handle *h, int32_t n, bool stream, const uint8_t *images,
+                                 int64_t pitch_bytes, const float *flow, const uint8_t *flow_valid,
+                                 const sgm_camera *cam, const sgm_sceneflow_out *out, void *stream_) {
     if (!h || !images || !flow || !out || !out->sf || !out->valid_sf) return SGM_ERR_INVALID_ARGUMENT;
-    if (n < 1 || n > h->prm.max_batch) return SGM_ERR_INVALID_ARGUMENT;
+    if (!batch_ok(h, n, stream)) return SGM_ERR_INVALID_ARGUMENT;
     if (pitch_bytes < h->prm.width || (pitch_bytes % 16) != 0 || !aligned16(images) ||
         !aligned16(out->sf) || (out->p0 && !aligned16(out->p0)) || (out->dp && !aligned16(out->dp)) ||
         (reinterpret_cast<uintptr_t>(flow) & 7))
         return SGM_ERR_INVALID_ARGUMENT;
-    return scene_flow_impl(h, n, images, pitch_bytes, flow, flow_valid, cam, out,
-                           static_cast<cudaStream_t>(stream));
+    return scene_flow_impl(h, n, stream, images, pitch_bytes, flow, flow_valid, cam, out,
+                           static_cast<cudaStream_t>(stream_));
 }
 
-sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, const float *flow,
-                               const uint8_t *flow_valid, const sgm_camera *cam,
-                               const sgm_sceneflow_out *out, void *stream) {
+sgm_status sgm_scene_flow(sgm_handle *h, int32_t n, const uint8_t *images, int64_t pitch_bytes,
+                          const float *flow, const uint8_t *flow_valid, const sgm_camera *cam,
+                          const sgm_sceneflow_out *out, void *stream) {
+    return scene_flow_dev(h, n, false, images, pitch_bytes, flow, flow_valid, cam, out, stream);
+}
+
+sgm_status sgm_scene_flow_stream(sgm_handle *h, int32_t n, const uint8_t *images, int64_t pitch_bytes,
+                                 const float *flow, const uint8_t *flow_valid, const sgm_camera *cam,
+                                 const sgm_sceneflow_out *out, void *stream) {
+    return scene_flow_dev(h, n, true, images, pitch_bytes, flow, flow_valid, cam, out, stream);
+}
+
+static sgm_status scene_flow_host_impl(sgm_handle *h, int32_t n, bool stream_mode,
+                                       const uint8_t *images, const float *flow,
+                                       const uint8_t *flow_valid, const sgm_camera *cam,
+                                       const sgm_sceneflow_out *out, void *stream) {
     if (!h || !images || !flow || !out || !out->sf || !out->valid_sf) return SGM_ERR_INVALID_ARGUMENT;
-    if (n < 1 || n > h->prm.max_batch) return SGM_ERR_INVALID_ARGUMENT;
+    if (!batch_ok(h, n, stream_mode)) return SGM_ERR_INVALID_ARGUMENT;
+    const long long nimg = stream_mode ? 2LL * (n + 1) : 4LL * n;   // images in the batch
+    const long long nmaps = nimg / 2;                                // LR-checked maps
     const bool want3d = out->p0 || out->dp || out->valid_3d;
     if (want3d && (!out->dp || !out->valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -518,7 +541,7 @@ sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, 
     cudaError_t e = cudaSuccess;
     if (sg.used) e = cudaStreamWaitEvent(h->s_in, sg.ev_comp, 0);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(sg.img_dense, images, size_t(4LL * n * H * W), cudaMemcpyHostToDevice, h->s_in);
+        e = cudaMemcpyAsync(sg.img_dense, images, size_t(nimg * H * W), cudaMemcpyHostToDevice, h->s_in);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(sg.flow, flow, sizeof(float) * 2 * npx * n, cudaMemcpyHostToDevice, h->s_in);
     if (e == cudaSuccess && flow_valid)
@@ -526,7 +549,7 @@ sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, 
     if (e == cudaSuccess) e = cudaEventRecord(sg.ev_in, h->s_in);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(h->s_comp, sg.ev_in, 0);
     if (e == cudaSuccess && sg.used) e = cudaStreamWaitEvent(h->s_comp, sg.ev_out, 0);
-    if (e == cudaSuccess) e = sgm::launch_repitch(sg.img_dense, sg.img, W, h->stage_pitch, 4LL * n * H, h->s_comp);
+    if (e == cudaSuccess) e = sgm::launch_repitch(sg.img_dense, sg.img, W, h->stage_pitch, nimg * H, h->s_comp);
     if (e != cudaSuccess) { h->timing = timing; return from_cuda(e); }
     ++h->launches;
     sgm_sceneflow_out dev{};
@@ -534,8 +557,9 @@ sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, 
     dev.valid_sf = sg.vsf;
     if (want3d) { dev.p0 = out->p0 ? sg.p0 : nullptr; dev.dp = sg.dp; dev.valid_3d = sg.v3; }
     dev.disp_int = sg.di; dev.disp_sub = sg.ds; dev.disp_valid = sg.dv;
-    sgm_status s = scene_flow_impl(h, n, sg.img, h->stage_pitch, sg.flow, flow_valid ? sg.fvalid : nullptr,
-                                   cam, &dev, h->s_comp, 0, h->sync_host);
+    sgm_status s = scene_flow_impl(h, n, stream_mode, sg.img, h->stage_pitch, sg.flow,
+                                   flow_valid ? sg.fvalid : nullptr, cam, &dev, h->s_comp,
+                                   h->sync_host);
     h->timing = timing;
     if (s != SGM_OK) return s;
     sg.used = true;
@@ -551,12 +575,25 @@ sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, 
         d2h(out->dp, sg.dp, sizeof(float) * 4 * npx * n);
         d2h(out->valid_3d, sg.v3, size_t(npx) * n);
     }
-    d2h(out->disp_int, sg.di, sizeof(int16_t) * 2 * npx * n);
-    d2h(out->disp_sub, sg.ds, sizeof(float) * 2 * npx * n);
-    d2h(out->disp_valid, sg.dv, size_t(2 * npx) * n);
+    d2h(out->disp_int, sg.di, sizeof(int16_t) * npx * nmaps);
+    d2h(out->disp_sub, sg.ds, sizeof(float) * npx * nmaps);
+    d2h(out->disp_valid, sg.dv, size_t(npx) * nmaps);
     if (e == cudaSuccess) e = cudaEventRecord(sg.ev_out, h->s_out);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, sg.ev_out, 0);
     return from_cuda(e);
+}
+
+sgm_status sgm_scene_flow_host(sgm_handle *h, int32_t n, const uint8_t *images, const float *flow,
+                               const uint8_t *flow_valid, const sgm_camera *cam,
+                               const sgm_sceneflow_out *out, void *stream) {
+    return scene_flow_host_impl(h, n, false, images, flow, flow_valid, cam, out, stream);
+}
+
+sgm_status sgm_scene_flow_stream_host(sgm_handle *h, int32_t n, const uint8_t *images,
+                                      const float *flow, const uint8_t *flow_valid,
+                                      const sgm_camera *cam, const sgm_sceneflow_out *out,
+                                      void *stream) {
+    return scene_flow_host_impl(h, n, true, images, flow, flow_valid, cam, out, stream);
 }
 
 }  // extern "C"

@@ -164,7 +164,9 @@ class SGM:
         return {"sf": sf, "valid_sf": vsf, "p0": p0, "dp": dp, "valid_3d": v3}
 
     # ------------------------------------------------------------------ production path
-    def alloc_outputs(self, n, with_3d=True, with_disp=True, pinned_host=False, with_p0=True):
+    def alloc_outputs(self, n, with_3d=True, with_disp=True, pinned_host=False, with_p0=True,
+                      stream_mode=False):
+        """Output tensors for n quads.  stream_mode: disparities per frame, [n+1][H][W]."""
         H, W = self.H, self.W
         if pinned_host:
             mk = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True)  # noqa: E731
@@ -176,9 +178,9 @@ class SGM:
             if with_p0:
                 out["p0"] = mk((n, H, W, 4), torch.float32)
         if with_disp:
-            out.update(disp_int=mk((n, 2, H, W), torch.int16),
-                       disp_sub=mk((n, 2, H, W), torch.float32),
-                       disp_valid=mk((n, 2, H, W), torch.uint8))
+            shp = (n + 1, H, W) if stream_mode else (n, 2, H, W)
+            out.update(disp_int=mk(shp, torch.int16), disp_sub=mk(shp, torch.float32),
+                       disp_valid=mk(shp, torch.uint8))
         return out
 
     @staticmethod
@@ -194,6 +196,31 @@ class SGM:
         out = out if out is not None else self.alloc_outputs(n)
         o = self._out_struct(out)
         _lib.call("sgm_scene_flow", self.h, n, _ptr(images), int(images.stride(2)), _ptr(flow),
+                  _ptr(flow_valid), ctypes.byref(camera.c()), ctypes.byref(o), _stream(stream))
+        return out
+
+    def scene_flow_stream(self, images, flow, camera, out=None, flow_valid=None, stream=None):
+        """Streaming mode: images uint8 [n+1][2][H][pitch] device tensor (frame k =
+        I_l^k, I_r^k of one video); flow float32 [n][H][W][2] (frame k -> k+1).  Quad k =
+        (frame k, frame k+1); disparity outputs are per frame [n+1][H][W]."""
+        n = int(flow.shape[0])
+        if int(images.shape[0]) != n + 1:
+            raise ValueError("stream mode needs n+1 frames for n flows")
+        out = out if out is not None else self.alloc_outputs(n, stream_mode=True)
+        o = self._out_struct(out)
+        _lib.call("sgm_scene_flow_stream", self.h, n, _ptr(images), int(images.stride(2)),
+                  _ptr(flow), _ptr(flow_valid), ctypes.byref(camera.c()), ctypes.byref(o),
+                  _stream(stream))
+        return out
+
+    def scene_flow_stream_host(self, images, flow, camera, out, flow_valid=None, stream=None):
+        """Host-buffer streaming mode: images uint8 [n+1][2][H][W], flow [n][H][W][2] and
+        ``out`` (pinned) CPU tensors."""
+        n = int(flow.shape[0])
+        if int(images.shape[0]) != n + 1:
+            raise ValueError("stream mode needs n+1 frames for n flows")
+        o = self._out_struct(out)
+        _lib.call("sgm_scene_flow_stream_host", self.h, n, _ptr(images), _ptr(flow),
                   _ptr(flow_valid), ctypes.byref(camera.c()), ctypes.byref(o), _stream(stream))
         return out
 
@@ -232,6 +259,16 @@ def rates_from_counts(counts):
         r["density"] = 100.0 * n_ev / n_gt if n_gt else float("nan")
         out[name] = r
     return out
+
+
+def stack_video(video, pitch, device):
+    """synth.make_video dict -> device frames [n+1][2][H][pitch], flow [n][H][W][2]."""
+    left, right = video["left"], video["right"]
+    nf, H, W = left.shape
+    imgs = torch.zeros((nf, 2, H, pitch), dtype=torch.uint8)
+    imgs[:, 0, :, :W] = torch.from_numpy(left)
+    imgs[:, 1, :, :W] = torch.from_numpy(right)
+    return imgs.to(device), torch.from_numpy(video["flow"]).to(device)
 
 
 def stack_quads(quads, pitch, device):
