@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-eval", action="store_true", help="skip the evaluation-step timing")
+    ap.add_argument("--no-stream", action="store_true", help="skip the streaming-mode timing")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL gather of results")
     return ap.parse_args()
 
@@ -366,6 +367,35 @@ def main():
                "pipelined": "steps issued back to back; per-step upload/download overlap the "
                             "neighbouring steps' kernels"}
 
+    # ---------------- streaming (video) mode, timed on its own
+    # F consecutive quads of one video (F+1 frames): each frame's map computed once.
+    stream_res = None
+    if not args.no_stream:
+        from paper_1801_04720_b200 import stack_video
+        video = synth.make_video(cfg, F, idx[0])
+        vimgs, vflow = stack_video(video, sgm.pitch, dev)
+        vout = sgm.alloc_outputs(F, stream_mode=True)
+        with torch.cuda.stream(stream):
+            for _ in range(max(args.warmup, 3)):
+                sgm.scene_flow_stream(vimgs, vflow, cam, vout, stream=stream)
+            sv_ms = 0.0
+            for _ in range(args.steps):
+                flush_l2()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                sgm.scene_flow_stream(vimgs, vflow, cam, vout, stream=stream)
+                e1.record(stream)
+                e1.synchronize()
+                sv_ms += e0.elapsed_time(e1)
+        sv_ms = max_over_ranks(sv_ms, dev) / args.steps
+        stream_res = {"workload": f"one video of {F + 1} frames = {F} quads per GPU "
+                                  f"({F + 1} SGM pairs instead of {2 * F})",
+                      "ms_per_step": sv_ms, "frames_per_s": F * world / (sv_ms * 1e-3),
+                      "map_cells_per_s": (F + 1) * world * W * H * D / (sv_ms * 1e-3),
+                      "speedup_vs_quad_mode": ms_per_step / sv_ms}
+        del vimgs, vflow, vout
+
     # ---------------- the evaluation step, timed on its own
     # (not part of the step above): KITTI outlier counts of the step's scene flow
     # against the generator's ground truth, one sgm_evaluate launch per step.
@@ -447,6 +477,7 @@ def main():
             "cpu_baseline": cpu,
             "geometry": geo,
             "evaluate": evaluation,
+            "stream": stream_res,
         }
         if gather:
             line["gather"] = gather
