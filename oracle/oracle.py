@@ -15,6 +15,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sgm_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "flow_oracle.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -26,10 +27,11 @@ def lib_path() -> str:
 
 def build(force: bool = False) -> str:
     """Compile sgm_oracle.c with gcc -O2 -ffp-contract=off (no SIMD intrinsics)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or \
+            os.path.getmtime(_LIB) < max(os.path.getmtime(s) for s in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
-                               "-std=c11", "-o", tmp, _SRC, "-lm"])
+                               "-std=c11", "-o", tmp, *_SRCS, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -55,6 +57,22 @@ def _get():
                                           P, P, P, P, P, P, P]
             lib.orc_combine.argtypes = [P, P, P, P, P, P, I, I, I, P, P]
             lib.orc_reproject.argtypes = [P, P, I, I, Dd, Dd, Dd, Dd, P, P, P, P]
+            U64 = ctypes.c_uint64
+            lib.orc_ff_downsample.argtypes = [P, I, I, P]
+            lib.orc_ff_wht.argtypes = [P, I, I, I, P]
+            lib.orc_ff_patch_cost.argtypes = [P, P, I, I, I, I, I, I, I, I]
+            lib.orc_ff_patch_cost.restype = ctypes.c_int32
+            lib.orc_ff_knn_init.argtypes = [P, P, I, I, I, I, I, I, P, P, P]
+            lib.orc_ff_rng.argtypes = [U64, I, I, I, I]
+            lib.orc_ff_rng.restype = U64
+            lib.orc_ff_sweep.argtypes = [P, P, I, I, I, I, I, I, I, U64, P, P]
+            lib.orc_ff_lift.argtypes = [P, P, I, I, I, I, P, I, I, P, P]
+            lib.orc_ff_field.argtypes = [P, P, I, I, I, I, I, I, I, I, I, U64, P, P]
+            lib.orc_ff_consistency.argtypes = [P, P, P, I, I, I, P]
+            lib.orc_ff_flow.argtypes = [P, P, I, I, I, I, I, I, I, I, I, U64, I, P, P]
+            for fn in ("orc_ff_downsample", "orc_ff_wht", "orc_ff_knn_init", "orc_ff_sweep",
+                       "orc_ff_lift", "orc_ff_field", "orc_ff_consistency", "orc_ff_flow"):
+                getattr(lib, fn).restype = ctypes.c_int
             lib.orc_evaluate.argtypes = [P, P, P, P, P, P, P, I, I, ctypes.c_float, ctypes.c_float, P]
             for fn in ("orc_census", "orc_cost", "orc_path", "orc_aggregate", "orc_wta",
                        "orc_lr_check", "orc_sgm_view", "orc_disparity", "orc_combine",
@@ -272,3 +290,108 @@ def run_stream(video, prm, rule=0, threads=True):
         quads.append({"disp0": maps[k], "disp1": maps[k + 1], "sf": sf, "valid_sf": vsf,
                       "p0": p0, "p1": p1, "dp": dp, "valid_3d": v3})
     return {"maps": maps, "quads": quads}
+
+
+# ---------------------------------------------------------------- optical flow (flow_oracle.c)
+FQ = 8   # flow vectors are integers in 1/FQ px (reading FF1)
+
+FF_DEFAULTS = {"levels": 3, "r": 4, "sweeps": 8, "R0": 8, "win": 8, "knn": 4, "penalty": 20,
+               "seed": 1, "thr_q": 8}
+
+
+def ff_downsample(img):
+    img = _c(img, np.uint8)
+    H, W = img.shape
+    out = np.empty(((H + 1) // 2, (W + 1) // 2), np.uint8)
+    _chk(_get().orc_ff_downsample(_p(img), W, H, _p(out)), "ff_downsample")
+    return out
+
+
+def ff_wht(img, win=8):
+    img = _c(img, np.uint8)
+    H, W = img.shape
+    out = np.empty((H, W, 16), np.int32)
+    _chk(_get().orc_ff_wht(_p(img), W, H, win, _p(out)), "ff_wht")
+    return out
+
+
+def ff_patch_cost(A, B, x, y, fu, fv, r=4, penalty=20):
+    A = _c(A, np.uint8)
+    B = _c(B, np.uint8)
+    H, W = A.shape
+    return int(_get().orc_ff_patch_cost(_p(A), _p(B), W, H, x, y, fu, fv, r, penalty))
+
+
+def ff_knn_init(A, B, win=8, knn=4, r=4, penalty=20):
+    A = _c(A, np.uint8)
+    B = _c(B, np.uint8)
+    H, W = A.shape
+    flow = np.empty((H, W, 2), np.int32)
+    cost = np.empty((H, W), np.int32)
+    nn = np.empty((H, W, knn), np.int32)
+    _chk(_get().orc_ff_knn_init(_p(A), _p(B), W, H, win, knn, r, penalty, _p(flow), _p(cost),
+                                _p(nn)), "ff_knn_init")
+    return flow, cost, nn
+
+
+def ff_rng(seed, level, sweep, x, y):
+    return int(_get().orc_ff_rng(seed, level, sweep, x, y))
+
+
+def ff_sweep(A, B, flow, cost, sweep, level=0, r=4, penalty=20, R0=8, seed=1):
+    """One propagation sweep + random search, in place on copies (returned)."""
+    A = _c(A, np.uint8)
+    B = _c(B, np.uint8)
+    H, W = A.shape
+    flow = np.array(flow, np.int32, copy=True)
+    cost = np.array(cost, np.int32, copy=True)
+    _chk(_get().orc_ff_sweep(_p(A), _p(B), W, H, r, penalty, sweep, level, R0, seed,
+                             _p(flow), _p(cost)), "ff_sweep")
+    return flow, cost
+
+
+def ff_lift(A, B, coarse, r=4, penalty=20):
+    A = _c(A, np.uint8)
+    B = _c(B, np.uint8)
+    coarse = _c(coarse, np.int32)
+    H, W = A.shape
+    Hc, Wc = coarse.shape[:2]
+    flow = np.empty((H, W, 2), np.int32)
+    cost = np.empty((H, W), np.int32)
+    _chk(_get().orc_ff_lift(_p(A), _p(B), W, H, Wc, Hc, _p(coarse), r, penalty, _p(flow),
+                            _p(cost)), "ff_lift")
+    return flow, cost
+
+
+def ff_field(A, B, levels=3, r=4, sweeps=8, R0=8, win=8, knn=4, penalty=20, seed=1):
+    A = _c(A, np.uint8)
+    B = _c(B, np.uint8)
+    H, W = A.shape
+    flow = np.empty((H, W, 2), np.int32)
+    cost = np.empty((H, W), np.int32)
+    _chk(_get().orc_ff_field(_p(A), _p(B), W, H, levels, r, sweeps, R0, win, knn, penalty, seed,
+                             _p(flow), _p(cost)), "ff_field")
+    return flow, cost
+
+
+def ff_consistency(F, G1, G2, thr_q=8):
+    F = _c(F, np.int32)
+    G1 = _c(G1, np.int32)
+    G2 = _c(G2, np.int32)
+    H, W = F.shape[:2]
+    v = np.empty((H, W), np.uint8)
+    _chk(_get().orc_ff_consistency(_p(F), _p(G1), _p(G2), W, H, thr_q, _p(v)), "ff_consistency")
+    return v
+
+
+def ff_flow(A, B, levels=3, r=4, sweeps=8, R0=8, win=8, knn=4, penalty=20, seed=1, thr_q=8):
+    """Forward field + two inverse fields + consistency.  Returns (flow int32
+    [H][W][2] in 1/FQ px, valid uint8 [H][W])."""
+    A = _c(A, np.uint8)
+    B = _c(B, np.uint8)
+    H, W = A.shape
+    flow = np.empty((H, W, 2), np.int32)
+    v = np.empty((H, W), np.uint8)
+    _chk(_get().orc_ff_flow(_p(A), _p(B), W, H, levels, r, sweeps, R0, win, knn, penalty, seed,
+                            thr_q, _p(flow), _p(v)), "ff_flow")
+    return flow, v

@@ -385,3 +385,17 @@ def random_eval_instance(H, W, seed, n=None):
     noc = ((rng.random(shp) < 0.85) & (gv > 0)).astype(np.uint8)
     return {"sf": sf.astype(np.float32), "valid_sf": v, "gt_d0": gd0, "gt_d1": gd1,
             "gt_flow": gfl, "gt_noc": noc, "gt_valid": gv}
+
+
+def translated_pair(W, H, seed, tx, ty, sigma=1.0):
+    """Frames A, B of a textured plane translated by the integer (tx, ty): the point at x
+    in A appears at x + (tx, ty) in B, so the true flow A -> B is (tx, ty) wherever
+    x + (tx, ty) is inside the image ("exact-translation recovery")."""
+    rng = np.random.default_rng(seed)
+    m = 16 + max(abs(tx), abs(ty))
+    t = rng.uniform(0.0, 255.0, size=(H + 2 * m, W + 2 * m))
+    t = gaussian_filter(t, sigma=sigma, mode="reflect")
+    t = (t - t.min()) * (255.0 / max(t.max() - t.min(), 1e-9))
+    A = _round_u8(t[m:m + H, m:m + W])
+    B = _round_u8(t[m - ty:m - ty + H, m - tx:m - tx + W])
+    return A, B
