@@ -5,10 +5,14 @@ csrc/*.cu; ``SGM`` is its thin torch-tensor binding.  Importing this package
 does not touch the GPU; creating an ``SGM`` loads the library and fails loudly
 if it is missing (there is no CPU fallback).
 """
-__all__ = ["SGM", "Camera", "stack_quads", "pitch_for", "rates_from_counts", "stack_video"]
+__all__ = ["SGM", "Camera", "stack_quads", "pitch_for", "rates_from_counts", "stack_video",
+           "FlowFields"]
 
 
 def __getattr__(name):
+    if name == "FlowFields":
+        from . import flow
+        return flow.FlowFields
     if name in __all__:
         from . import sgm
         return getattr(sgm, name)

@@ -1,4 +1,4 @@
-"""ctypes binding of libsgmsf.so (include/sgmsf.h): argument marshalling only.
+"""ctypes binding of libsgmsf.so (include/sgmsf.h, include/sgmflow.h): argument marshalling only.
 
 Every step of the method runs in the library's CUDA kernels; this module turns
 Python ints / pointers into the C types of the ABI and raises on non-OK
@@ -19,13 +19,17 @@ STATUS = {0: "SGM_OK", 1: "SGM_ERR_INVALID_ARGUMENT", 2: "SGM_ERR_UNSUPPORTED", 
           4: "SGM_ERR_OUT_OF_MEMORY"}
 NUM_STAGES = 5
 
-# Every symbol include/sgmsf.h declares (checked by tests/test_abi.py).
+# Every symbol include/*.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "sgm_create", "sgm_destroy", "sgm_status_string", "sgm_census", "sgm_cost", "sgm_aggregate",
     "sgm_wta", "sgm_lr_check", "sgm_disparity", "sgm_combine_sceneflow", "sgm_scene_flow",
     "sgm_scene_flow_host", "sgm_set_timing", "sgm_read_timing", "sgm_stage_name",
     "sgm_launch_count", "sgm_get_geometry", "sgm_last_error_string", "sgm_debug_set_trace",
     "sgm_evaluate", "sgm_scene_flow_stream", "sgm_scene_flow_stream_host",
+    # include/sgmflow.h
+    "sgm_flow_create", "sgm_flow_destroy", "sgm_flow_last_error_string", "sgm_flow_launch_count",
+    "sgm_flow", "sgm_flow_field", "sgm_flow_descriptors", "sgm_flow_patch_cost",
+    "sgm_flow_knn_init", "sgm_flow_sweep", "sgm_flow_consistency",
 )
 
 
@@ -65,6 +69,15 @@ class SgmSceneflowOut(ctypes.Structure):
                 ("p0", ctypes.c_void_p), ("dp", ctypes.c_void_p),
                 ("valid_3d", ctypes.c_void_p), ("disp_int", ctypes.c_void_p),
                 ("disp_sub", ctypes.c_void_p), ("disp_valid", ctypes.c_void_p)]
+
+
+class SgmFlowParams(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32), ("levels", ctypes.c_int32),
+                ("patch_radius", ctypes.c_int32), ("sweeps", ctypes.c_int32),
+                ("search_radius", ctypes.c_int32), ("desc_window", ctypes.c_int32),
+                ("knn", ctypes.c_int32), ("consistency_q", ctypes.c_int32),
+                ("penalty", ctypes.c_int32), ("max_batch", ctypes.c_int32),
+                ("seed", ctypes.c_uint64)]
 
 
 _lib = None
@@ -118,6 +131,17 @@ def load(path: str | None = None):
         "sgm_debug_set_trace": (st, [P, P]),
         "sgm_get_geometry": (st, [P, ctypes.POINTER(I32), ctypes.POINTER(I32),
                                   ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+        "sgm_flow_create": (st, [ctypes.POINTER(SgmFlowParams), I32, ctypes.POINTER(P)]),
+        "sgm_flow_destroy": (None, [P]),
+        "sgm_flow_last_error_string": (ctypes.c_char_p, []),
+        "sgm_flow_launch_count": (I64, [P]),
+        "sgm_flow": (st, [P, I32, P, P, P, P, P, P]),
+        "sgm_flow_field": (st, [P, I32, P, P, ctypes.c_uint64, I32, P, P, P]),
+        "sgm_flow_descriptors": (st, [P, P, I32, I32, P, P]),
+        "sgm_flow_patch_cost": (st, [P, P, P, I32, I32, I32, I32, P, P, P]),
+        "sgm_flow_knn_init": (st, [P, P, P, I32, I32, I32, P, P, P, P]),
+        "sgm_flow_sweep": (st, [P, P, P, I32, I32, I32, I32, I32, ctypes.c_uint64, P, P, P]),
+        "sgm_flow_consistency": (st, [P, P, P, P, I32, I32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

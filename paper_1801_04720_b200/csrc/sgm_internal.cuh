@@ -80,6 +80,19 @@ struct EvalParams {
     unsigned *ticket;                      // zero between launches (the last block resets it)
 };
 
+// Optical-flow fields of a batch (flow.cu): pair k's level images A_k = A + k img_stride,
+// B_k = B + k img_stride; field f = k fpp + kind (kind 0: A->B; 1, 2: B->A, F-5).
+struct FFFields {
+    int W, H, fpp, nfields;
+    const uint8_t *A, *B;
+    long long img_stride;
+    int radius[3];
+    uint64_t seed[3];
+    int penalty;
+    int32_t *flow;                 // [nfields][H][W][2] (1/8 px)
+    int32_t *cost;                 // [nfields][H][W]
+};
+
 // ----------------------------------------------------------------- launchers (host)
 cudaError_t launch_census(const uint8_t *const *imgs, int nimg, long long pitch, int W, int H,
                           int cw, int ch, uint64_t *out, long long out_stride, cudaStream_t st);
@@ -96,5 +109,21 @@ cudaError_t launch_repitch(const uint8_t *src, uint8_t *dst, int W, long long pi
 cudaError_t launch_combine(const CombineParams &p, cudaStream_t st);
 cudaError_t launch_evaluate(const EvalParams &p, cudaStream_t st);
 int evaluate_max_blocks();   // scratch rows launch_evaluate may use besides one per quad
+cudaError_t ff_launch_downsample(const uint8_t *src, long long src_stride, int W, int H, uint8_t *dst,
+                                 long long dst_stride, int nimg, cudaStream_t st);
+cudaError_t ff_launch_wht(const uint8_t *img, long long img_stride, int W, int H, int win, int nimg,
+                          int32_t *desc, cudaStream_t st);
+cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int32_t *nn, cudaStream_t st);
+cudaError_t ff_launch_init(const FFFields &F, const int32_t *nn, int knn, cudaStream_t st);
+cudaError_t ff_launch_lift(const FFFields &F, const int32_t *coarse, int Wc, int Hc, cudaStream_t st);
+cudaError_t ff_launch_sweep(const FFFields &F, int sweep, int level, int R0, int *sync, cudaStream_t st,
+                            int *launches);
+int ff_sync_ints(int nfields, int H);
+size_t ff_prop_smem(int W);
+cudaError_t ff_launch_consistency(const int32_t *F, const int32_t *G1, const int32_t *G2, long long fstride,
+                                  long long gstride, int W, int H, int n, int thr_q, uint8_t *valid,
+                                  float *fout, cudaStream_t st);
+cudaError_t ff_launch_cost_query(const uint8_t *A, const uint8_t *B, int W, int H, int r, int penalty, int nq,
+                                 const int32_t *q, int32_t *out, cudaStream_t st);
 
 }  // namespace sgm

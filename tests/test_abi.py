@@ -1,5 +1,5 @@
 """Host-side checks of the C-ABI library (no GPU needed): it loads, exports every
-symbol include/sgmsf.h declares, and rejects invalid parameters synchronously
+symbol include/*.h declares, and rejects invalid parameters synchronously
 before touching the device."""
 import ctypes
 import os
@@ -13,8 +13,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def header_symbols():
-    src = open(os.path.join(ROOT, "include", "sgmsf.h")).read()
-    return sorted(set(re.findall(r"^SGM_API[^(]*?\b(sgm_\w+)\s*\(", src, flags=re.M)))
+    syms = set()
+    inc = os.path.join(ROOT, "include")
+    for name in sorted(os.listdir(inc)):
+        if name.endswith(".h"):
+            src = open(os.path.join(inc, name)).read()
+            syms |= set(re.findall(r"^SGM_API[^(]*?\b(sgm_\w+)\s*\(", src, flags=re.M))
+    return sorted(syms)
 
 
 def test_header_declares_documented_entry_points():
@@ -73,6 +78,10 @@ def test_null_handle_calls_are_rejected():
     assert lib.sgm_evaluate(None, 1, None, None, None, None, None, None, None, 3.0, 0.05,
                             None, None) == 1
     assert lib.sgm_launch_count(None) == 0
+    assert lib.sgm_flow(None, 1, None, None, None, None, None, None) == 1
+    assert lib.sgm_flow_field(None, 1, None, None, 0, 4, None, None, None) == 1
+    assert lib.sgm_flow_launch_count(None) == 0
+    lib.sgm_flow_destroy(None)
     lib.sgm_destroy(None)
 
 
@@ -82,3 +91,22 @@ def test_no_fallback_when_library_missing(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib._build, "NVCC", str(tmp_path / "no-nvcc"))
     with pytest.raises(_lib.SgmLibraryError):
         _lib.load(str(tmp_path / "libsgmsf.so"))
+
+
+FLOW_OK = dict(width=64, height=48, levels=3, patch_radius=4, sweeps=8, search_radius=8,
+               desc_window=8, knn=4, consistency_q=8, penalty=20, max_batch=1, seed=1)
+
+
+@pytest.mark.parametrize("field,value", [("width", 0), ("levels", 0), ("levels", 9),
+                                         ("patch_radius", 6), ("patch_radius", -1),
+                                         ("search_radius", 0), ("desc_window", 6), ("knn", 0),
+                                         ("knn", 9), ("penalty", 256), ("max_batch", 0),
+                                         ("width", 100000)])
+def test_flow_create_rejects_invalid_params(field, value):
+    lib = _lib.load()
+    kw = dict(FLOW_OK)
+    kw[field] = value
+    p = _lib.SgmFlowParams(**kw)
+    h = ctypes.c_void_p()
+    assert lib.sgm_flow_create(ctypes.byref(p), 0, ctypes.byref(h)) == 1
+    assert h.value is None
