@@ -69,6 +69,17 @@ SGM_API sgm_status sgm_flow(sgm_flow_handle *h, int32_t n, const uint8_t *frames
                     const uint8_t *frames1, float *flow, uint8_t *valid, int32_t *fields_q,
                     void *stream);
 
+/* ---- instrumentation ------------------------------------------------------ */
+enum { SGM_FLOW_NUM_STAGES = 3 };   /* propagation, random search, kNN */
+
+/* Enable (1) / disable (0) CUDA-event timing of the propagation, random-search and kNN
+ * kernels of every following sgm_flow / sgm_flow_field call (events on the call's stream). */
+SGM_API sgm_status sgm_flow_set_timing(sgm_flow_handle *h, int32_t enable);
+
+/* Summed kernel time (ms) per stage of the last timed call into ms[SGM_FLOW_NUM_STAGES]
+ * (waits for its events); returns the number of stages written, 0 if nothing was timed. */
+SGM_API int32_t sgm_flow_read_timing(sgm_flow_handle *h, float *ms);
+
 /* ---- stage-wise entry points (parity tests, debugging) ------------------- */
 
 /* One match field per pair, A_k -> B_k, through the whole pyramid with (seed, radius):

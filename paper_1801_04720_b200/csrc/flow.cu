@@ -17,10 +17,10 @@
 //                         image row, the row's pixels in scan order; the warp's 32 lanes
 //                         split the (2r+1)^2 samples of both candidates (left/up, or
 //                         right/down) and sum them with REDUX; rows hand their vectors to the
-//                         next row through shared memory (per-pixel progress counter), bands
-//                         of NW rows hand over through global memory (release/acquire
-//                         progress flag every kPubFF pixels); CTAs take tickets so a band only
-//                         waits for an already-running band
+//                         next row through a shared-memory ring, bands of NW rows through a
+//                         global row buffer, both as tagged 64-bit words polled directly (no
+//                         fences); CTAs take tickets so a band only waits for an
+//                         already-running band
 //   ff_search_kernel      the random search after each sweep (thread per pixel, counter RNG)
 //   ff_lift_kernel        x2 vectors, nearest-neighbour upsampling, costs recomputed
 //   ff_consistency_kernel two-inverse-field check (thread per pixel)
@@ -31,36 +31,73 @@ namespace {
 
 constexpr int FQ = 8;
 constexpr int FQ2 = FQ * FQ;
-constexpr int kPubFF = 8;        // band-handoff publication granularity (pixels)
-constexpr int kNsMax = 8;        // samples per lane: (2r+1)^2 <= 256 -> r <= 7
+constexpr int kRowRing = 128;    // row -> next-row handoff ring (positions) per warp
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-// |Q^2 a - bilinear B| of one sample, or the penalty outside B (FF4).
-__device__ __forceinline__ int sample_cost(const uint8_t *__restrict__ B, int W, int H, int px, int py,
-                                           int a, int pen64) {
-    if (px < 0 || py < 0 || px > (W - 1) * FQ || py > (H - 1) * FQ) return pen64;
-    const int ix = px >> 3, fx = px & 7, iy = py >> 3, fy = py & 7;
-    const int ix1 = min(ix + 1, W - 1), iy1 = min(iy + 1, H - 1);
-    const uint8_t *r0 = B + (long long)iy * W, *r1 = B + (long long)iy1 * W;
-    const int b = (FQ - fx) * (FQ - fy) * int(__ldg(r0 + ix)) + fx * (FQ - fy) * int(__ldg(r0 + ix1)) +
-                  (FQ - fx) * fy * int(__ldg(r1 + ix)) + fx * fy * int(__ldg(r1 + ix1));
-    return abs(FQ2 * a - b);
-}
+// Quad image (FF4 helper, exact): Q(x, y) packs the four bilinear taps B(x, y), B(x+1, y),
+// B(x, y+1), B(x+1, y+1) (coordinates clamped) into one 32-bit word, so a sample is one
+// load and one DP4A against the packed weights.
+// Bilinear setup of one candidate vector (fu, fv): every sample of the patch has the same
+// fractional part, so the weights and the integer offset are computed once.  Sample at
+// pixel (sx, sy) reads Q at (sx + qx, sy + qy); it lies inside [0, (W-1) Q] x [0, (H-1) Q]
+// iff 0 <= sx + qx <= ixmax and 0 <= sy + qy <= iymax (a clamped tap has weight 0).
+struct Cand {
+    int qx, qy, ixmax, iymax;
+    unsigned wpack;
+    __device__ __forceinline__ Cand(int fu, int fv, int W, int H) {
+        qx = fu >> 3; qy = fv >> 3;                    // floor (arithmetic shift)
+        const int fx = fu & 7, fy = fv & 7;
+        wpack = unsigned((FQ - fx) * (FQ - fy)) | (unsigned(fx * (FQ - fy)) << 8) |
+                (unsigned((FQ - fx) * fy) << 16) | (unsigned(fx * fy) << 24);
+        ixmax = W - 1 - (fx ? 1 : 0); iymax = H - 1 - (fy ? 1 : 0);
+    }
+    // |Q^2 a - b| at B position (ix, iy) = sample + (qx, qy), or pen64 outside
+    __device__ __forceinline__ int cost(const uint32_t *__restrict__ QB, int W, int ix, int iy, int a,
+                                        int pen64) const {
+        const bool in = (ix | iy) >= 0 && ix <= ixmax && iy <= iymax;
+        const unsigned t = __ldg(QB + (in ? (long long)iy * W + ix : 0));
+        const int b = int(__dp4a(t, wpack, 0u));
+        return in ? abs(FQ2 * a - b) : pen64;
+    }
+};
 
-// The whole data term by one thread, sample order irrelevant (integers).
-__device__ int patch_cost_thread(const uint8_t *__restrict__ A, const uint8_t *__restrict__ B, int W,
-                                 int H, int x, int y, int fu, int fv, int r, int pen64) {
+// The whole data term by one thread, sample order irrelevant (integers).  The
+// row loop is unrolled over the widest supported patch (15) with a predicate, so the
+// loads of a row's samples are in flight together.
+__device__ __forceinline__ int patch_cost_thread(const uint8_t *__restrict__ A, const uint32_t *__restrict__ QB,
+                                                 int W, int H, int x, int y, int fu, int fv, int r, int pen64) {
+    const Cand c(fu, fv, W, H);
     int s = 0;
     for (int dy = -r; dy <= r; ++dy) {
         const uint8_t *arow = A + (long long)clampi(y + dy, 0, H - 1) * W;
-        const int py = (y + dy) * FQ + fv;
-        for (int dx = -r; dx <= r; ++dx) {
-            const int a = __ldg(arow + clampi(x + dx, 0, W - 1));
-            s += sample_cost(B, W, H, (x + dx) * FQ + fu, py, a, pen64);
+        const int iy = y + dy + c.qy;
+#pragma unroll
+        for (int k = 0; k < 15; ++k) {
+            const int dx = k - r;
+            if (dx <= r) {
+                const int a = __ldg(arow + clampi(x + dx, 0, W - 1));
+                s += c.cost(QB, W, x + dx + c.qx, iy, a, pen64);
+            }
         }
     }
     return s;
+}
+
+__global__ void ff_quad_kernel(const uint8_t *__restrict__ src, long long src_stride, int W, int H, int nimg,
+                               uint32_t *__restrict__ dst, long long dst_stride) {
+    const long long per = (long long)W * H, total = per * nimg;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int k = int(t / per);
+        const long long q = t - k * per;
+        const int y = int(q / W), x = int(q - (long long)y * W);
+        const uint8_t *s0 = src + k * src_stride + (long long)y * W;
+        const uint8_t *s1 = src + k * src_stride + (long long)min(y + 1, H - 1) * W;
+        const int x1 = min(x + 1, W - 1);
+        dst[k * dst_stride + q] = unsigned(s0[x]) | (unsigned(s0[x1]) << 8) | (unsigned(s1[x]) << 16) |
+                                  (unsigned(s1[x1]) << 24);
+    }
 }
 
 __device__ __forceinline__ uint64_t splitmix(uint64_t seed, int level, int sweep, int x, int y) {
@@ -144,55 +181,75 @@ constexpr int kKnnTile = 128;
 // image p and its database from image p ^ 1 (A_k -> B_k, B_k -> A_k); nn [nprob][n][knn]
 __global__ void __launch_bounds__(128) ff_knn_kernel(const int32_t *__restrict__ desc, int n, int knn,
                                                      int32_t *__restrict__ nn) {
-    __shared__ int4 tile[kKnnTile * 4];
+    __shared__ double tile[kKnnTile][16];
     const int prob = blockIdx.y;
     const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = qi < n;
     const int32_t *dq = desc + (long long)prob * n * 16;
     const int32_t *dd = desc + (long long)(prob ^ 1) * n * 16;
     double q[16];
-    if (qi < n) {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) q[c] = double(dq[(long long)qi * 16 + c]);
-    }
+    for (int c = 0; c < 16; ++c) q[c] = active ? double(dq[(long long)qi * 16 + c]) : 0.0;
     double bd[kKnnMax];
     int bi[kKnnMax];
 #pragma unroll
     for (int k = 0; k < kKnnMax; ++k) { bd[k] = 1e300; bi[k] = 0x7fffffff; }
-    for (int base = 0; base < n; base += kKnnTile) {
+    double thr = active ? 1e300 : -1.0;           // k-th best distance so far (inactive: never)
+    int thr_i = 0x7fffffff;                        // and its index
+    // Tiles are visited nearest-first around the block's own image position (small motions
+    // find good matches early, so the DC bound prunes most of the database).  Entries are
+    // ranked by (distance, index) lexicographically, so the visiting order does not change
+    // the result: it equals the index-order scan of the oracle with ties to the smaller index.
+    const int ntiles = (n + kKnnTile - 1) / kKnnTile;
+    const int t0 = min(int((long long)blockIdx.x * blockDim.x / kKnnTile), ntiles - 1);
+    for (int it = 0; it < ntiles; ++it) {
+        // t0, t0+1, t0-1, t0+2, t0-2, ... clipped to [0, ntiles)
+        const int up = ntiles - 1 - t0, dn = t0;
+        int t;
+        const int h = (it + 1) / 2;
+        if (it == 0) t = t0;
+        else if (h <= min(up, dn)) t = (it & 1) ? t0 + h : t0 - h;
+        else t = up > dn ? t0 + (it - dn) : t0 - (it - up);
+        const int base = t * kKnnTile;
         __syncthreads();
-        for (int t = threadIdx.x; t < kKnnTile * 4; t += blockDim.x) {
-            const int e = base + t / 4;
-            tile[t] = e < n ? reinterpret_cast<const int4 *>(dd)[(long long)e * 4 + (t & 3)] : make_int4(0, 0, 0, 0);
+        for (int u = threadIdx.x; u < kKnnTile * 16; u += blockDim.x) {
+            const int e = base + u / 16;
+            tile[u / 16][u & 15] = e < n ? double(dd[(long long)e * 16 + (u & 15)]) : 0.0;
         }
         __syncthreads();
-        if (qi >= n) continue;
         const int lim = min(kKnnTile, n - base);
         for (int e = 0; e < lim; ++e) {
-            double d = 0.0;
+            // the DC term alone bounds the distance from below: when it exceeds the k-th
+            // best for every lane, the entry cannot enter any list (exact pruning)
+            const double t0d = q[0] - tile[e][0];
+            double d = t0d * t0d;
+            if (!__any_sync(0xffffffffu, d <= thr)) continue;
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-                const int4 v = tile[e * 4 + c4];
-                double t0 = q[4 * c4] - double(v.x), t1 = q[4 * c4 + 1] - double(v.y);
-                double t2 = q[4 * c4 + 2] - double(v.z), t3 = q[4 * c4 + 3] - double(v.w);
-                d = fma(t0, t0, d); d = fma(t1, t1, d); d = fma(t2, t2, d); d = fma(t3, t3, d);
+            for (int c = 1; c < 16; ++c) {
+                const double tc = q[c] - tile[e][c];
+                d = fma(tc, tc, d);
             }
             // exact: every term and partial sum is an integer < 2^53
-            if (d < bd[knn - 1]) {
-                int idx = base + e;
+            const int idx = base + e;
+            if (d < thr || (d == thr && idx < thr_i)) {
+                int ci = idx;
                 double dv = d;
                 bool ins = false;
 #pragma unroll
-                for (int k = 0; k < kKnnMax; ++k) {      // sorted insertion after equal keys;
-                    if (k < knn && (ins || dv < bd[k])) {   // displaced entries shift down
+                for (int k = 0; k < kKnnMax; ++k) {      // sorted insertion by (d, index)
+                    if (k < knn && (ins || dv < bd[k] || (dv == bd[k] && ci < bi[k]))) {
                         const double td = bd[k]; const int ti = bi[k];
-                        bd[k] = dv; bi[k] = idx; dv = td; idx = ti;
+                        bd[k] = dv; bi[k] = ci; dv = td; ci = ti;
                         ins = true;
                     }
                 }
+#pragma unroll
+                for (int k = 0; k < kKnnMax; ++k)
+                    if (k == knn - 1) { thr = bd[k]; thr_i = bi[k]; }
             }
         }
     }
-    if (qi < n)
+    if (active)
         for (int k = 0; k < knn; ++k) nn[((long long)prob * n + qi) * knn + k] = bi[k];
 }
 
@@ -203,18 +260,23 @@ struct FieldSet {
     int W, H, fpp, nfields;
     const uint8_t *A, *B;          // level images, pair k at + k * img_stride
     long long img_stride;
+    const uint32_t *QA, *QB;       // their quad images, pair k at + k * img_stride
     int radius[3];
     uint64_t seed[3];
     int pen64;
     int32_t *flow;                 // [nfields][H][W][2]
     int32_t *cost;                 // [nfields][H][W]
-    __device__ __forceinline__ void images(int f, const uint8_t *&src, const uint8_t *&dst) const {
+    // source image and the quad image of the target of field f
+    __device__ __forceinline__ void images(int f, const uint8_t *&src, const uint32_t *&qdst) const {
         const int k = f / fpp, kind = f - k * fpp;
-        const uint8_t *a = A + k * img_stride, *b = B + k * img_stride;
-        src = kind == 0 ? a : b;
-        dst = kind == 0 ? b : a;
+        src = (kind == 0 ? A : B) + k * img_stride;
+        qdst = (kind == 0 ? QB : QA) + k * img_stride;
     }
     __device__ __forceinline__ int kind(int f) const { return f % fpp; }
+    // selects instead of indexing: a runtime index into the by-value parameter arrays
+    // would copy them to local memory
+    __device__ __forceinline__ int rad(int k) const { return k == 0 ? radius[0] : (k == 1 ? radius[1] : radius[2]); }
+    __device__ __forceinline__ uint64_t sd(int k) const { return k == 0 ? seed[0] : (k == 1 ? seed[1] : seed[2]); }
 };
 
 // best of the k candidates (FF5): nn lists per (pair, direction): direction 0 = A->B
@@ -225,7 +287,8 @@ __global__ void ff_init_kernel(FieldSet fs, const int32_t *__restrict__ nn, int 
         const int f = int(t / per);
         const long long p = t - f * per;
         const int y = int(p / fs.W), x = int(p - (long long)y * fs.W);
-        const uint8_t *src, *dst;
+        const uint8_t *src;
+        const uint32_t *dst;
         fs.images(f, src, dst);
         const int kind = fs.kind(f), pair = f / fs.fpp;
         const int dir = kind == 0 ? 0 : 1;
@@ -235,7 +298,7 @@ __global__ void ff_init_kernel(FieldSet fs, const int32_t *__restrict__ nn, int 
             const int q = cand[k];
             const int yb = q / fs.W, xb = q - yb * fs.W;
             const int fu = (xb - x) * FQ, fv = (yb - y) * FQ;
-            const int c = patch_cost_thread(src, dst, fs.W, fs.H, x, y, fu, fv, fs.radius[kind], fs.pen64);
+            const int c = patch_cost_thread(src, dst, fs.W, fs.H, x, y, fu, fv, fs.rad(kind), fs.pen64);
             if (c < best) { best = c; bu = fu; bv = fv; }
         }
         fs.flow[2 * t] = bu;
@@ -255,11 +318,12 @@ __global__ void ff_lift_kernel(FieldSet fs, const int32_t *__restrict__ coarse, 
         const int y = int(p / fs.W), x = int(p - (long long)y * fs.W);
         const long long c = f * cper + (long long)min(y >> 1, Hc - 1) * Wc + min(x >> 1, Wc - 1);
         const int fu = 2 * coarse[2 * c], fv = 2 * coarse[2 * c + 1];
-        const uint8_t *src, *dst;
+        const uint8_t *src;
+        const uint32_t *dst;
         fs.images(f, src, dst);
         fs.flow[2 * t] = fu;
         fs.flow[2 * t + 1] = fv;
-        fs.cost[t] = patch_cost_thread(src, dst, fs.W, fs.H, x, y, fu, fv, fs.radius[fs.kind(f)], fs.pen64);
+        fs.cost[t] = patch_cost_thread(src, dst, fs.W, fs.H, x, y, fu, fv, fs.rad(fs.kind(f)), fs.pen64);
     }
 }
 
@@ -274,12 +338,13 @@ __global__ void ff_search_kernel(FieldSet fs, int sweep, int level, int R0) {
         const long long p = t - f * per;
         const int y = int(p / fs.W), x = int(p - (long long)y * fs.W);
         const int kind = fs.kind(f);
-        const uint64_t z = splitmix(fs.seed[kind], level, sweep, x, y);
+        const uint64_t z = splitmix(fs.sd(kind), level, sweep, x, y);
         const int fu = fs.flow[2 * t] + int(unsigned(z) % span) - R * FQ;
         const int fv = fs.flow[2 * t + 1] + int(unsigned(z >> 32) % span) - R * FQ;
-        const uint8_t *src, *dst;
+        const uint8_t *src;
+        const uint32_t *dst;
         fs.images(f, src, dst);
-        const int c = patch_cost_thread(src, dst, fs.W, fs.H, x, y, fu, fv, fs.radius[kind], fs.pen64);
+        const int c = patch_cost_thread(src, dst, fs.W, fs.H, x, y, fu, fv, fs.rad(kind), fs.pen64);
         if (c < fs.cost[t]) {
             fs.cost[t] = c;
             fs.flow[2 * t] = fu;
@@ -289,31 +354,162 @@ __global__ void ff_search_kernel(FieldSet fs, int sweep, int level, int R0) {
 }
 
 // ------------------------------------------------------------------ propagation (FF7)
-__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_gpu(int *p, int v) {
-    asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-
 struct PropParams {
     FieldSet fs;
     int sweep;
     int nbands;
-    int *ticket;       // zeroed before the launch
-    int *progress;     // [nfields][nbands], zeroed before the launch
+    int *ticket;                  // zeroed before the launch
+    unsigned long long *hand;     // [nfields][nbands][W] band handoff rows, zeroed before the launch
 };
+
+// Row-to-row handoff entries: one 64-bit word = vector (2 x 20-bit two's complement, 1/8 px)
+// + tag (24 bits, position + 1, 0 = empty).  A 64-bit store / load is single-copy atomic,
+// so the consumer polls the entry itself: no fence and no separate progress flag.
+__device__ __forceinline__ unsigned long long pack_hand(int u, int v, int tag) {
+    return (unsigned long long)(unsigned(u) & 0xFFFFFu) | ((unsigned long long)(unsigned(v) & 0xFFFFFu) << 20) |
+           ((unsigned long long)unsigned(tag) << 40);
+}
+__device__ __forceinline__ int hand_tag(unsigned long long e) { return int(e >> 40); }
+__device__ __forceinline__ int2 hand_vec(unsigned long long e) {
+    const int u = int(unsigned(e) << 12) >> 12;                     // sign-extend 20 bits
+    const int v = int(unsigned(e >> 20) << 12) >> 12;
+    return make_int2(u, v);
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+
+// One row of one field in scan order (the body of ff_prop_kernel); NK = samples per lane
+// ((2r+1)^2 <= 32 NK), so every lane's A and B loads of a pixel are issued together.
+template <int NW, int NK>
+__device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned long long *sring,
+                                         volatile int *sprog, int f, int band, int warp, int lane, int j) {
+    const FieldSet &fs = pp.fs;
+    const int W = fs.W, H = fs.H;
+    const bool fwd = (pp.sweep & 1) == 0;
+    const int y = fwd ? j : H - 1 - j;
+    const uint8_t *src;
+    const uint32_t *dst;
+    fs.images(f, src, dst);
+    const int kind = fs.kind(f);
+    const int r = fs.rad(kind), side = 2 * r + 1, ns = side * side;
+    const long long per = (long long)W * H;
+    int32_t *flow = fs.flow + 2 * f * per;
+    int32_t *cost = fs.cost + f * per;
+    const bool has_above = j > 0;                   // previous row in scan order exists
+    const bool above_in_cta = warp > 0;
+    const bool has_below_in_cta = warp + 1 < NW && j + 1 < H;
+    // band handoff rows: [nfields][nbands][W], zeroed before the launch
+    const unsigned long long *hin = pp.hand + ((long long)f * pp.nbands + band - 1) * W;
+    unsigned long long *hout = pp.hand + ((long long)f * pp.nbands + band) * W;
+    const bool publish = warp == NW - 1 && band + 1 < pp.nbands;
+    volatile unsigned long long *ring_in = sring + (size_t)(warp - 1) * kRowRing;
+    volatile unsigned long long *ring_out = sring + (size_t)warp * kRowRing;
+    // this lane's samples: (dx, dy) of sample lane + 32 k, valid iff < ns
+    int sdx[NK], sdy[NK];
+    bool sok[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        const int sidx = lane + 32 * k;
+        sok[k] = sidx < ns;
+        const int q = sok[k] ? sidx : 0;
+        sdy[k] = q / side - r;
+        sdx[k] = q - (q / side) * side - r;
+    }
+    long long aoff[NK];                             // A row of each of this lane's samples
+#pragma unroll
+    for (int k = 0; k < NK; ++k) aoff[k] = (long long)clampi(y + sdy[k], 0, H - 1) * W;
+    int2 hv = make_int2(0, 0);                      // vector of the previous pixel in scan order
+    // incumbent of the next position, loaded one position ahead
+    int nx0 = fwd ? 0 : W - 1;
+    long long np = (long long)y * W + nx0;
+    int ncu = flow[2 * np], ncv = flow[2 * np + 1], ncc = cost[np];
+    for (int i = 0; i < W; ++i) {
+        const int x = fwd ? i : W - 1 - i;
+        const long long p = (long long)y * W + x;
+        int cu = ncu, cv = ncv, cc = ncc;
+        if (i + 1 < W) {
+            np = p + (fwd ? 1 : -1);
+            ncu = flow[2 * np]; ncv = flow[2 * np + 1]; ncc = cost[np];
+        }
+        int a[NK];
+#pragma unroll
+        for (int k = 0; k < NK; ++k)
+            a[k] = __ldg(src + aoff[k] + clampi(x + sdx[k], 0, W - 1));
+        // vertical candidate: the finished vector of (x, row above in scan order)
+        int2 vv = make_int2(0, 0);
+        if (has_above) {
+            unsigned long long e;
+            if (above_in_cta) {
+                // back off while waiting: spinning warps would take the issue slots of the
+                // warps that have work
+                while (hand_tag(e = ring_in[i & (kRowRing - 1)]) != i + 1) __nanosleep(20);
+            } else {
+                while (hand_tag(e = ld_relaxed_u64(hin + i)) != i + 1) __nanosleep(32);
+            }
+            vv = hand_vec(e);
+        }
+        // candidates in order: horizontal (previous pixel), vertical; skip ones equal to
+        // the incumbent (their data term equals the incumbent's: never strictly better)
+        const bool eh = i > 0 && (hv.x != cu || hv.y != cv);
+        const bool ev = has_above && (vv.x != cu || vv.y != cv) && (!eh || vv.x != hv.x || vv.y != hv.y);
+        if (eh && ev) {                             // both candidates: loads in flight together
+            const Cand C0(hv.x, hv.y, W, H), C1(vv.x, vv.y, W, H);
+            int s0 = 0, s1 = 0;
+#pragma unroll
+            for (int k = 0; k < NK; ++k) {
+                const int sx = x + sdx[k], sy = y + sdy[k];
+                const int t0 = C0.cost(dst, W, sx + C0.qx, sy + C0.qy, a[k], fs.pen64);
+                const int t1 = C1.cost(dst, W, sx + C1.qx, sy + C1.qy, a[k], fs.pen64);
+                s0 += sok[k] ? t0 : 0;
+                s1 += sok[k] ? t1 : 0;
+            }
+            const int c0 = int(__reduce_add_sync(0xffffffffu, unsigned(s0)));
+            const int c1 = int(__reduce_add_sync(0xffffffffu, unsigned(s1)));
+            if (c0 < cc) { cc = c0; cu = hv.x; cv = hv.y; }
+            if (c1 < cc) { cc = c1; cu = vv.x; cv = vv.y; }
+        } else if (eh || ev) {                      // one candidate
+            const int2 w = eh ? hv : vv;
+            const Cand C0(w.x, w.y, W, H);
+            int s0 = 0;
+#pragma unroll
+            for (int k = 0; k < NK; ++k) {
+                const int t0 = C0.cost(dst, W, x + sdx[k] + C0.qx, y + sdy[k] + C0.qy, a[k], fs.pen64);
+                s0 += sok[k] ? t0 : 0;
+            }
+            const int c0 = int(__reduce_add_sync(0xffffffffu, unsigned(s0)));
+            if (c0 < cc) { cc = c0; cu = w.x; cv = w.y; }
+        }
+        if (lane == 0) {
+            if (has_below_in_cta) {
+                // ring slot reuse: the row below must have consumed position i - kRowRing
+                if (i >= kRowRing)
+                    while (sprog[warp + 1] < i - kRowRing + 1) __nanosleep(20);
+                ring_out[i & (kRowRing - 1)] = pack_hand(cu, cv, i + 1);
+            }
+            if (publish) st_relaxed_u64(hout + i, pack_hand(cu, cv, i + 1));
+            sprog[warp] = i + 1;
+            flow[2 * p] = cu;
+            flow[2 * p + 1] = cv;
+            cost[p] = cc;
+        }
+        hv = make_int2(cu, cv);
+        __syncwarp();
+    }
+}
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) ff_prop_kernel(const PropParams pp) {
-    const FieldSet &fs = pp.fs;
-    const int W = fs.W, H = fs.H;
     extern __shared__ __align__(16) unsigned char ff_smem[];
-    int2 *srow = reinterpret_cast<int2 *>(ff_smem);          // [NW][W]
-    volatile int *sprog = reinterpret_cast<volatile int *>(srow + (size_t)NW * W);   // [NW]
+    volatile unsigned long long *sring = reinterpret_cast<volatile unsigned long long *>(ff_smem);   // [NW][kRowRing]
+    volatile int *sprog = reinterpret_cast<volatile int *>(ff_smem + sizeof(unsigned long long) * NW * kRowRing);
     __shared__ int s_ticket;
+    for (int t = threadIdx.x; t < NW * kRowRing; t += blockDim.x) sring[t] = 0ull;
     if (threadIdx.x < NW) sprog[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_ticket = atomicAdd(pp.ticket, 1);
     __syncthreads();
@@ -321,84 +517,13 @@ __global__ void __launch_bounds__(NW * 32) ff_prop_kernel(const PropParams pp) {
     const int f = ticket / pp.nbands, band = ticket - f * pp.nbands;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = band * NW + warp;                 // iteration row
-    if (j >= H) return;
-    const bool fwd = (pp.sweep & 1) == 0;
-    const int y = fwd ? j : H - 1 - j;
-    const uint8_t *src, *dst;
-    fs.images(f, src, dst);
-    const int kind = fs.kind(f);
-    const int r = fs.radius[kind], side = 2 * r + 1, ns = side * side;
-    const long long per = (long long)W * H;
-    int32_t *flow = fs.flow + 2 * f * per;
-    int32_t *cost = fs.cost + f * per;
-    const bool has_above = j > 0;                   // previous row in scan order exists
-    const bool above_in_cta = warp > 0;
-    const int *prog_in = pp.progress + f * pp.nbands + band - 1;
-    int *prog_out = pp.progress + f * pp.nbands + band;
-    const bool publish = warp == NW - 1 && band + 1 < pp.nbands;
-    const int yv = fwd ? y - 1 : y + 1;             // row of the vertical candidate
-    int known = 0;
-    int2 hv = make_int2(0, 0);                      // vector of the previous pixel in scan order
-    for (int i = 0; i < W; ++i) {
-        const int x = fwd ? i : W - 1 - i;
-        const long long p = (long long)y * W + x;
-        int cu = flow[2 * p], cv = flow[2 * p + 1], cc = cost[p];
-        // vertical candidate: the finished vector of (x, yv)
-        int2 vv = make_int2(0, 0);
-        if (has_above) {
-            if (above_in_cta) {
-                while (sprog[warp - 1] < i + 1) { }
-                const volatile int *sv = reinterpret_cast<const volatile int *>(srow + (size_t)(warp - 1) * W + x);
-                vv = make_int2(sv[0], sv[1]);
-            } else {
-                if (known < i + 1) {
-                    int k;
-                    while ((k = ld_acquire_gpu(prog_in)) < min(i + 1, W)) __nanosleep(20);
-                    known = k;
-                }
-                const long long q = (long long)yv * W + x;
-                vv = make_int2(__ldcg(flow + 2 * q), __ldcg(flow + 2 * q + 1));
-            }
-        }
-        // candidates in order: horizontal (previous pixel), vertical; skip ones equal to
-        // the incumbent (their data term equals the incumbent's: never strictly better)
-        const bool eh = i > 0 && (hv.x != cu || hv.y != cv);
-        bool ev = has_above && (vv.x != cu || vv.y != cv) && (!eh || vv.x != hv.x || vv.y != hv.y);
-        if (eh || ev) {
-            int s0 = 0, s1 = 0;
-            for (int k = 0; k < kNsMax; ++k) {
-                const int sidx = lane + 32 * k;
-                if (sidx < ns) {
-                    const int dy = sidx / side - r, dx = sidx - (sidx / side) * side - r;
-                    const int a = __ldg(src + (long long)clampi(y + dy, 0, H - 1) * W + clampi(x + dx, 0, W - 1));
-                    const int bx = (x + dx) * FQ, by = (y + dy) * FQ;
-                    if (eh) s0 += sample_cost(dst, W, H, bx + hv.x, by + hv.y, a, fs.pen64);
-                    if (ev) s1 += sample_cost(dst, W, H, bx + vv.x, by + vv.y, a, fs.pen64);
-                }
-            }
-            if (eh) {
-                const int c0 = int(__reduce_add_sync(0xffffffffu, unsigned(s0)));
-                if (c0 < cc) { cc = c0; cu = hv.x; cv = hv.y; }
-            }
-            if (ev) {
-                const int c1 = int(__reduce_add_sync(0xffffffffu, unsigned(s1)));
-                if (c1 < cc) { cc = c1; cu = vv.x; cv = vv.y; }
-            }
-        }
-        if (lane == 0) {
-            flow[2 * p] = cu;
-            flow[2 * p + 1] = cv;
-            cost[p] = cc;
-            srow[(size_t)warp * W + x] = make_int2(cu, cv);
-        }
-        hv = make_int2(cu, cv);
-        if (lane == 0) {
-            __threadfence_block();
-            sprog[warp] = i + 1;
-            if (publish && ((i + 1) % kPubFF == 0 || i == W - 1)) st_release_gpu(prog_out, i + 1);
-        }
-        __syncwarp();
-    }
+    if (j >= pp.fs.H) return;
+    const int r = pp.fs.rad(pp.fs.kind(f));
+    const int nk = ((2 * r + 1) * (2 * r + 1) + 31) / 32;
+    if (nk <= 1) prop_row<NW, 1>(pp, sring, sprog, f, band, warp, lane, j);
+    else if (nk <= 3) prop_row<NW, 3>(pp, sring, sprog, f, band, warp, lane, j);
+    else if (nk <= 6) prop_row<NW, 6>(pp, sring, sprog, f, band, warp, lane, j);
+    else prop_row<NW, 8>(pp, sring, sprog, f, band, warp, lane, j);
 }
 
 // ------------------------------------------------------------------ consistency (FF9)
@@ -440,10 +565,10 @@ __global__ void ff_consistency_kernel(const int32_t *__restrict__ F, const int32
 }
 
 // data term of explicit queries (parity / debugging)
-__global__ void ff_cost_query_kernel(const uint8_t *A, const uint8_t *B, int W, int H, int r, int pen64,
+__global__ void ff_cost_query_kernel(const uint8_t *A, const uint32_t *QB, int W, int H, int r, int pen64,
                                      int nq, const int32_t *q, int32_t *out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nq) out[i] = patch_cost_thread(A, B, W, H, q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3], r, pen64);
+    if (i < nq) out[i] = patch_cost_thread(A, QB, W, H, q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3], r, pen64);
 }
 
 int ff_grid(long long n, int block) {
@@ -479,6 +604,7 @@ static FieldSet make_fs(const FFFields &F) {
     FieldSet fs{};
     fs.W = F.W; fs.H = F.H; fs.fpp = F.fpp; fs.nfields = F.nfields;
     fs.A = F.A; fs.B = F.B; fs.img_stride = F.img_stride;
+    fs.QA = F.QA; fs.QB = F.QB;
     for (int k = 0; k < 3; ++k) { fs.radius[k] = F.radius[k]; fs.seed[k] = F.seed[k]; }
     fs.pen64 = F.penalty * FQ2;
     fs.flow = F.flow; fs.cost = F.cost;
@@ -497,33 +623,44 @@ cudaError_t ff_launch_lift(const FFFields &F, const int32_t *coarse, int Wc, int
     return cudaGetLastError();
 }
 
-constexpr int kPropNW = 8;
+constexpr int kPropNW = 16;
 
-size_t ff_prop_smem(int W) { return size_t(kPropNW) * W * sizeof(int2) + 64; }
+size_t ff_prop_smem(int W) {
+    (void)W;
+    return size_t(kPropNW) * kRowRing * sizeof(unsigned long long) + 64 * sizeof(int);
+}
 
 cudaError_t ff_launch_sweep(const FFFields &F, int sweep, int level, int R0, int *sync, cudaStream_t st,
-                            int *launches) {
+                            int *launches, FFTimer *timer) {
     PropParams pp{};
     pp.fs = make_fs(F);
     pp.sweep = sweep;
     pp.nbands = (F.H + kPropNW - 1) / kPropNW;
     pp.ticket = sync;
-    pp.progress = sync + 1;
-    cudaError_t e = cudaMemsetAsync(sync, 0, sizeof(int) * (1 + size_t(F.nfields) * pp.nbands), st);
+    pp.hand = reinterpret_cast<unsigned long long *>(sync + 4);
+    const size_t hand_bytes = sizeof(unsigned long long) * size_t(F.nfields) * pp.nbands * F.W;
+    cudaError_t e = cudaMemsetAsync(sync, 0, 4 * sizeof(int) + hand_bytes, st);
     if (e != cudaSuccess) return e;
     const size_t sm = ff_prop_smem(F.W);
     e = cudaFuncSetAttribute(ff_prop_kernel<kPropNW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     if (e != cudaSuccess) return e;
+    if (timer) timer->begin(0);
     ff_prop_kernel<kPropNW><<<F.nfields * pp.nbands, kPropNW * 32, sm, st>>>(pp);
+    if (timer) timer->end();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const long long n = (long long)F.W * F.H * F.nfields;
+    if (timer) timer->begin(1);
     ff_search_kernel<<<ff_grid(n, 128), 128, 0, st>>>(pp.fs, sweep, level, R0);
+    if (timer) timer->end();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (launches) *launches += 2;
     return cudaSuccess;
 }
 
-int ff_sync_ints(int nfields, int H) { return 1 + nfields * ((H + kPropNW - 1) / kPropNW); }
+// ticket (+ padding to 16 bytes) and the band handoff rows of the largest level
+long long ff_sync_ints(int nfields, int W, int H) {
+    return 4 + 2LL * nfields * ((H + kPropNW - 1) / kPropNW) * W;
+}
 
 cudaError_t ff_launch_consistency(const int32_t *F, const int32_t *G1, const int32_t *G2, long long fstride,
                                   long long gstride, int W, int H, int n, int thr_q, uint8_t *valid,
@@ -533,9 +670,16 @@ cudaError_t ff_launch_consistency(const int32_t *F, const int32_t *G1, const int
     return cudaGetLastError();
 }
 
-cudaError_t ff_launch_cost_query(const uint8_t *A, const uint8_t *B, int W, int H, int r, int penalty, int nq,
+cudaError_t ff_launch_cost_query(const uint8_t *A, const uint32_t *QB, int W, int H, int r, int penalty, int nq,
                                  const int32_t *q, int32_t *out, cudaStream_t st) {
-    ff_cost_query_kernel<<<(nq + 127) / 128, 128, 0, st>>>(A, B, W, H, r, penalty * FQ2, nq, q, out);
+    ff_cost_query_kernel<<<(nq + 127) / 128, 128, 0, st>>>(A, QB, W, H, r, penalty * FQ2, nq, q, out);
+    return cudaGetLastError();
+}
+
+cudaError_t ff_launch_quad(const uint8_t *src, long long src_stride, int W, int H, int nimg, uint32_t *dst,
+                           long long dst_stride, cudaStream_t st) {
+    ff_quad_kernel<<<ff_grid((long long)W * H * nimg, 256), 256, 0, st>>>(src, src_stride, W, H, nimg, dst,
+                                                                          dst_stride);
     return cudaGetLastError();
 }
 

@@ -14,13 +14,20 @@ struct sgm_flow_handle {
     long long pyr_off[8] = {};       // offset of level l in a pyramid buffer (per image)
     long long pyr_img = 0;           // bytes of one image's pyramid
     uint8_t *pyr = nullptr;          // [max_batch][2][pyr_img]: level images of A_k, B_k
+    uint32_t *quad = nullptr;        // [max_batch][2][pyr_img]: their quad images (same offsets)
     int32_t *desc = nullptr;         // [2 max_batch][Wc Hc][16]
     int32_t *nn = nullptr;           // [2 max_batch][Wc Hc][knn]
     int32_t *flow[2] = {nullptr, nullptr};   // ping-pong [3 max_batch][W H][2]
     int32_t *cost[2] = {nullptr, nullptr};   // [3 max_batch][W H]
     int *sync = nullptr;             // ticket + band progress of the propagation kernel
-    int32_t *query = nullptr;        // scratch for sgm_flow_patch_cost (device copy)
     long long launches = 0;
+    // instrumentation: event pairs around every launch of a category (prop, search, knn,
+    // other) of the last timed sgm_flow / sgm_flow_field call
+    bool timing = false;
+    static constexpr int kMaxEv = 256;
+    cudaEvent_t ev[kMaxEv] = {};
+    int ev_cat[kMaxEv / 2] = {};
+    int nev = 0;
 };
 
 namespace {
@@ -41,10 +48,29 @@ cudaError_t ff_alloc(T **p, size_t count) {
 }
 
 void ff_free(sgm_flow_handle *h) {
-    void *ptrs[] = {h->pyr, h->desc, h->nn, h->flow[0], h->flow[1], h->cost[0], h->cost[1], h->sync};
+    void *ptrs[] = {h->pyr, h->quad, h->desc, h->nn, h->flow[0], h->flow[1], h->cost[0], h->cost[1], h->sync};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    for (auto &e : h->ev)
+        if (e) cudaEventDestroy(e);
 }
+
+// timing helpers: mark(cat) before a launch, done() after it
+struct Timer : sgm::FFTimer {
+    sgm_flow_handle *h;
+    cudaStream_t st;
+    Timer(sgm_flow_handle *h_, cudaStream_t st_) : h(h_), st(st_) {}
+    void begin(int cat) override {
+        if (!h->timing || h->nev + 2 > sgm_flow_handle::kMaxEv) return;
+        h->ev_cat[h->nev / 2] = cat;
+        cudaEventRecord(h->ev[h->nev], st);
+    }
+    void end() override {
+        if (!h->timing || h->nev + 2 > sgm_flow_handle::kMaxEv) return;
+        cudaEventRecord(h->ev[h->nev + 1], st);
+        h->nev += 2;
+    }
+};
 
 bool params_ok(const sgm_flow_params *p) {
     if (!p) return false;
@@ -69,10 +95,18 @@ cudaError_t run_fields(sgm_flow_handle *h, int n, int fpp, uint64_t seed, int ra
     const sgm_flow_params &P = h->prm;
     const int L = P.levels;
     cudaError_t e = cudaSuccess;
+    Timer T(h, st);
+    if (h->timing) h->nev = 0;
     // pyramid of the 2n images (A_k, B_k interleaved, one pyramid per image)
     for (int l = 1; l < L && e == cudaSuccess; ++l) {
         e = sgm::ff_launch_downsample(h->pyr + h->pyr_off[l - 1], h->pyr_img, h->lw[l - 1], h->lh[l - 1],
                                       h->pyr + h->pyr_off[l], h->pyr_img, 2 * n, st);
+        if (e == cudaSuccess) ++h->launches;
+    }
+    // quad images of every level (the data term reads them)
+    for (int l = 0; l < L && e == cudaSuccess; ++l) {
+        e = sgm::ff_launch_quad(h->pyr + h->pyr_off[l], h->pyr_img, h->lw[l], h->lh[l], 2 * n,
+                                h->quad + h->pyr_off[l], h->pyr_img, st);
         if (e == cudaSuccess) ++h->launches;
     }
     if (e != cudaSuccess) return e;
@@ -82,7 +116,9 @@ cudaError_t run_fields(sgm_flow_handle *h, int n, int fpp, uint64_t seed, int ra
                            h->desc, st);
     if (e != cudaSuccess) return e;
     ++h->launches;
+    T.begin(2);
     e = sgm::ff_launch_knn(h->desc, int(h->lper[c]), 2 * n, P.knn, h->nn, st);
+    T.end();
     if (e != cudaSuccess) return e;
     ++h->launches;
     sgm::FFFields F{};
@@ -97,6 +133,8 @@ cudaError_t run_fields(sgm_flow_handle *h, int n, int fpp, uint64_t seed, int ra
         F.W = h->lw[l]; F.H = h->lh[l];
         F.A = h->pyr + h->pyr_off[l];
         F.B = F.A + h->pyr_img;
+        F.QA = h->quad + h->pyr_off[l];
+        F.QB = F.QA + h->pyr_img;
         F.flow = h->flow[cur]; F.cost = h->cost[cur];
         if (l == c) {
             e = sgm::ff_launch_init(F, h->nn, P.knn, st);
@@ -106,7 +144,8 @@ cudaError_t run_fields(sgm_flow_handle *h, int n, int fpp, uint64_t seed, int ra
         if (e == cudaSuccess) ++h->launches;
         for (int s = 0; s < P.sweeps && e == cudaSuccess; ++s) {
             int nl = 0;
-            e = sgm::ff_launch_sweep(F, s, l, P.search_radius, h->sync, st, &nl);
+            e = sgm::ff_launch_sweep(F, s, l, P.search_radius, h->sync, st, &nl,
+                                     h->timing ? &T : nullptr);
             h->launches += nl;
         }
         cur ^= 1;
@@ -149,13 +188,16 @@ sgm_status sgm_flow_create(const sgm_flow_params *p, int32_t device, sgm_flow_ha
     const size_t mb = size_t(p->max_batch);
     const size_t n0 = size_t(h->lper[0]), nc = size_t(h->lper[p->levels - 1]);
     if (e == cudaSuccess) e = ff_alloc(&h->pyr, mb * 2 * size_t(h->pyr_img));
+    if (e == cudaSuccess) e = ff_alloc(&h->quad, mb * 2 * size_t(h->pyr_img));
     if (e == cudaSuccess) e = ff_alloc(&h->desc, 2 * mb * nc * 16);
     if (e == cudaSuccess) e = ff_alloc(&h->nn, 2 * mb * nc * size_t(p->knn));
     for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
         e = ff_alloc(&h->flow[k], 3 * mb * n0 * 2);
         if (e == cudaSuccess) e = ff_alloc(&h->cost[k], 3 * mb * n0);
     }
-    if (e == cudaSuccess) e = ff_alloc(&h->sync, size_t(sgm::ff_sync_ints(3 * p->max_batch, p->height)));
+    if (e == cudaSuccess) e = ff_alloc(&h->sync, size_t(sgm::ff_sync_ints(3 * p->max_batch, p->width, p->height)));
+    for (auto &ev : h->ev)
+        if (e == cudaSuccess) e = cudaEventCreate(&ev);
     if (e != cudaSuccess) {
         sgm_status s = ff_status(e);
         ff_free(h);
@@ -177,6 +219,26 @@ void sgm_flow_destroy(sgm_flow_handle *h) {
 
 int64_t sgm_flow_launch_count(sgm_flow_handle *h) { return h ? h->launches : 0; }
 
+sgm_status sgm_flow_set_timing(sgm_flow_handle *h, int32_t enable) {
+    if (!h) return SGM_ERR_INVALID_ARGUMENT;
+    h->timing = enable != 0;
+    h->nev = 0;
+    return SGM_OK;
+}
+
+int32_t sgm_flow_read_timing(sgm_flow_handle *h, float *ms) {
+    if (!h || !ms || h->nev == 0) return 0;
+    for (int k = 0; k < SGM_FLOW_NUM_STAGES; ++k) ms[k] = 0.f;
+    for (int i = 0; i < h->nev; i += 2) {
+        float t = 0.f;
+        if (cudaEventSynchronize(h->ev[i + 1]) != cudaSuccess ||
+            cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]) != cudaSuccess)
+            return 0;
+        ms[h->ev_cat[i / 2]] += t;
+    }
+    return SGM_FLOW_NUM_STAGES;
+}
+
 sgm_status sgm_flow_descriptors(sgm_flow_handle *h, const uint8_t *img, int32_t w, int32_t hgt,
                                 int32_t *desc, void *stream) {
     if (!h || !img || !desc || w < 1 || hgt < 1) return SGM_ERR_INVALID_ARGUMENT;
@@ -193,9 +255,12 @@ sgm_status sgm_flow_patch_cost(sgm_flow_handle *h, const uint8_t *A, const uint8
     if (!h || !A || !B || !queries || !out || w < 1 || hgt < 1 || nq < 0 || radius < 0 || radius > 7)
         return SGM_ERR_INVALID_ARGUMENT;
     if (nq == 0) return SGM_OK;
-    cudaError_t e = sgm::ff_launch_cost_query(A, B, w, hgt, radius, h->prm.penalty, nq, queries, out,
-                                              static_cast<cudaStream_t>(stream));
-    if (e == cudaSuccess) ++h->launches;
+    if ((long long)w * hgt > h->lper[0]) return SGM_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = sgm::ff_launch_quad(B, 0, w, hgt, 1, h->quad, 0, st);
+    if (e == cudaSuccess)
+        e = sgm::ff_launch_cost_query(A, h->quad, w, hgt, radius, h->prm.penalty, nq, queries, out, st);
+    if (e == cudaSuccess) h->launches += 2;
     return ff_status(e);
 }
 
@@ -210,15 +275,17 @@ sgm_status sgm_flow_knn_init(sgm_flow_handle *h, const uint8_t *A, const uint8_t
     // images into the scratch pyramid slot 0 as one "pair" (A, B), level-0 layout
     cudaError_t e = cudaMemcpyAsync(h->pyr, A, size_t(n), cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(h->pyr + h->pyr_img, B, size_t(n), cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = sgm::ff_launch_quad(h->pyr, h->pyr_img, w, hgt, 2, h->quad, h->pyr_img, st);
     if (e == cudaSuccess) e = sgm::ff_launch_wht(h->pyr, h->pyr_img, w, hgt, h->prm.desc_window, 2, h->desc, st);
     if (e == cudaSuccess) e = sgm::ff_launch_knn(h->desc, int(n), 1, h->prm.knn, nn ? nn : h->nn, st);
     sgm::FFFields F{};
     F.W = w; F.H = hgt; F.fpp = 1; F.nfields = 1;
     F.A = h->pyr; F.B = h->pyr + h->pyr_img; F.img_stride = 2 * h->pyr_img;
+    F.QA = h->quad; F.QB = h->quad + h->pyr_img;
     F.radius[0] = radius; F.penalty = h->prm.penalty;
     F.flow = flow_q; F.cost = cost;
     if (e == cudaSuccess) e = sgm::ff_launch_init(F, nn ? nn : h->nn, h->prm.knn, st);
-    if (e == cudaSuccess) h->launches += 3;
+    if (e == cudaSuccess) h->launches += 4;
     return ff_status(e);
 }
 
@@ -228,15 +295,18 @@ sgm_status sgm_flow_sweep(sgm_flow_handle *h, const uint8_t *A, const uint8_t *B
     if (!h || !A || !B || !flow_q || !cost || w < 1 || hgt < 1 || radius < 0 || radius > 7 || sweep < 0 ||
         level < 0)
         return SGM_ERR_INVALID_ARGUMENT;
-    if (hgt > h->prm.height || sgm::ff_prop_smem(w) > 200 * 1024) return SGM_ERR_INVALID_ARGUMENT;
+    if (hgt > h->prm.height || w > h->prm.width) return SGM_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     sgm::FFFields F{};
     F.W = w; F.H = hgt; F.fpp = 1; F.nfields = 1;
     F.A = A; F.B = B; F.img_stride = 0;
+    F.QA = h->quad; F.QB = h->quad + h->pyr_img;       // scratch slots of pair 0
     F.radius[0] = radius; F.seed[0] = seed; F.penalty = h->prm.penalty;
     F.flow = flow_q; F.cost = cost;
-    int nl = 0;
-    cudaError_t e = sgm::ff_launch_sweep(F, sweep, level, h->prm.search_radius, h->sync,
-                                         static_cast<cudaStream_t>(stream), &nl);
+    cudaError_t e = sgm::ff_launch_quad(A, 0, w, hgt, 1, h->quad, 0, st);
+    if (e == cudaSuccess) e = sgm::ff_launch_quad(B, 0, w, hgt, 1, h->quad + h->pyr_img, 0, st);
+    int nl = 2;
+    if (e == cudaSuccess) e = sgm::ff_launch_sweep(F, sweep, level, h->prm.search_radius, h->sync, st, &nl);
     h->launches += nl;
     return ff_status(e);
 }

@@ -85,7 +85,8 @@ struct EvalParams {
 struct FFFields {
     int W, H, fpp, nfields;
     const uint8_t *A, *B;
-    long long img_stride;
+    long long img_stride;          // elements between pairs (also for QA / QB)
+    const uint32_t *QA, *QB;       // quad images of A, B (flow.cu ff_quad_kernel)
     int radius[3];
     uint64_t seed[3];
     int penalty;
@@ -116,14 +117,21 @@ cudaError_t ff_launch_wht(const uint8_t *img, long long img_stride, int W, int H
 cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int32_t *nn, cudaStream_t st);
 cudaError_t ff_launch_init(const FFFields &F, const int32_t *nn, int knn, cudaStream_t st);
 cudaError_t ff_launch_lift(const FFFields &F, const int32_t *coarse, int Wc, int Hc, cudaStream_t st);
+// stage timer of the flow handle (flow_api.cu): begin(category) / end() around a launch
+struct FFTimer {
+    virtual void begin(int cat) = 0;
+    virtual void end() = 0;
+};
 cudaError_t ff_launch_sweep(const FFFields &F, int sweep, int level, int R0, int *sync, cudaStream_t st,
-                            int *launches);
-int ff_sync_ints(int nfields, int H);
+                            int *launches, FFTimer *timer = nullptr);
+long long ff_sync_ints(int nfields, int W, int H);
 size_t ff_prop_smem(int W);
 cudaError_t ff_launch_consistency(const int32_t *F, const int32_t *G1, const int32_t *G2, long long fstride,
                                   long long gstride, int W, int H, int n, int thr_q, uint8_t *valid,
                                   float *fout, cudaStream_t st);
-cudaError_t ff_launch_cost_query(const uint8_t *A, const uint8_t *B, int W, int H, int r, int penalty, int nq,
+cudaError_t ff_launch_cost_query(const uint8_t *A, const uint32_t *QB, int W, int H, int r, int penalty, int nq,
                                  const int32_t *q, int32_t *out, cudaStream_t st);
+cudaError_t ff_launch_quad(const uint8_t *src, long long src_stride, int W, int H, int nimg, uint32_t *dst,
+                           long long dst_stride, cudaStream_t st);
 
 }  // namespace sgm

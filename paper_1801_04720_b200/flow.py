@@ -45,6 +45,16 @@ class FlowFields:
     def launch_count(self) -> int:
         return int(self.lib.sgm_flow_launch_count(self.h))
 
+    def set_timing(self, on: bool):
+        _lib.call("sgm_flow_set_timing", self.h, 1 if on else 0)
+
+    def read_timing(self):
+        """{prop, search, knn} summed kernel ms of the last timed call, or None."""
+        buf = (ctypes.c_float * 3)()
+        if self.lib.sgm_flow_read_timing(self.h, buf) == 0:
+            return None
+        return {"prop": float(buf[0]), "search": float(buf[1]), "knn": float(buf[2])}
+
     def _empty(self, shape, dtype):
         return torch.empty(shape, dtype=dtype, device=self.device)
 
