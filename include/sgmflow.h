@@ -37,7 +37,7 @@ extern "C" {
 #endif
 
 typedef struct sgm_flow_params {
-    int32_t width, height;    /* level-0 image size, >= 1 (width <= ~3200: row buffers) */
+    int32_t width, height;    /* level-0 image size, 1..16384 */
     int32_t levels;           /* pyramid levels 1..8 (SPEC default 3) */
     int32_t patch_radius;     /* r: (2r+1)^2 patch; r + 2 <= 7 (the second inverse field) (4) */
     int32_t sweeps;           /* propagation + random-search sweeps per level, 0..64 (8) */

@@ -74,15 +74,14 @@ struct Timer : sgm::FFTimer {
 
 bool params_ok(const sgm_flow_params *p) {
     if (!p) return false;
-    if (p->width < 1 || p->height < 1 || p->levels < 1 || p->levels > 8) return false;
+    // the row handoff packs vectors into 20-bit fields (+-65536 px in 1/8 px)
+    if (p->width < 1 || p->height < 1 || p->width > 16384 || p->height > 16384) return false;
+    if (p->levels < 1 || p->levels > 8) return false;
     if (p->patch_radius < 0 || p->patch_radius + 2 > 7) return false;    // r+2 <= 7 (256 samples)
     if (p->sweeps < 0 || p->sweeps > 64 || p->search_radius < 1) return false;
     if (p->desc_window != 4 && p->desc_window != 8 && p->desc_window != 16) return false;
     if (p->knn < 1 || p->knn > 8 || p->consistency_q < 0 || p->penalty < 0 || p->penalty > 255) return false;
     if (p->max_batch < 1) return false;
-    // the coarsest level must hold at least one pixel per dimension (always true) and the
-    // level-0 row must fit the propagation kernel's shared-memory row buffers
-    if (sgm::ff_prop_smem(p->width) > 200 * 1024) return false;
     return true;
 }
 
