@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-eval", action="store_true", help="skip the evaluation-step timing")
     ap.add_argument("--no-stream", action="store_true", help="skip the streaming-mode timing")
+    ap.add_argument("--no-flow", action="store_true", help="skip the optical-flow timing")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL gather of results")
     return ap.parse_args()
 
@@ -396,6 +397,82 @@ def main():
                       "speedup_vs_quad_mode": ms_per_step / sv_ms}
         del vimgs, vflow, vout
 
+    # ---------------- the optical-flow step (Flow Fields+-style
+    # core) timed on its own, and the full method: flow estimated on the GPU, then the
+    # scene-flow step with the estimated flow and its consistency mask.
+    flow_res = None
+    if not args.no_flow:
+        from paper_1801_04720_b200 import FlowFields
+        ffh = FlowFields(W, H, max_batch=F, device=local)
+        fa = imgs[:, 0, :, :W].contiguous()            # left frames t
+        fb = imgs[:, 2, :, :W].contiguous()            # left frames t+1
+        fo = ffh.flow(fa, fb, stream=stream)
+        sfo = sgm.alloc_outputs(F, with_disp=False)
+        fsteps = max(1, min(args.steps, 5))
+        with torch.cuda.stream(stream):
+            for _ in range(max(args.warmup, 3)):
+                ffh.flow(fa, fb, out=fo, stream=stream)
+            stream.synchronize()
+
+            def timed(fn):
+                tot = 0.0
+                for _ in range(fsteps):
+                    flush_l2()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    fn()
+                    e1.record(stream)
+                    e1.synchronize()
+                    tot += e0.elapsed_time(e1)
+                return max_over_ranks(tot, dev) / fsteps
+
+            f_ms = timed(lambda: ffh.flow(fa, fb, out=fo, stream=stream))
+            full_ms = timed(lambda: (ffh.flow(fa, fb, out=fo, stream=stream),
+                                     sgm.scene_flow(imgs, fo["flow"], cam, sfo, flow_valid=fo["valid"],
+                                                    stream=stream)))
+            ffh.set_timing(True)
+            ffh.flow(fa, fb, out=fo, stream=stream)
+            stream.synchronize()
+            fstages = ffh.read_timing()
+            ffh.set_timing(False)
+        gtf = flow.cpu().numpy()
+        estf = fo["flow"].cpu().numpy()
+        fval = fo["valid"].cpu().numpy() > 0
+        epe = np.hypot(estf[..., 0] - gtf[..., 0], estf[..., 1] - gtf[..., 1])
+        # roofline of the propagation kernel: the method's work per sweep is two candidate
+        # data terms per pixel, (2r+1)^2 samples x 8 integer ops (4 bilinear multiply-adds,
+        # Q^2 a, subtract, abs, accumulate); the kernel is a latency-bound wavefront
+        P = ffh.params
+        ops = 0.0
+        lw, lh = W, H
+        for _lvl in range(P.levels):
+            for r in (P.patch_radius, P.patch_radius, P.patch_radius + 2):
+                ops += F * lw * lh * P.sweeps * 2 * (2 * r + 1) ** 2 * 8
+            lw, lh = (lw + 1) // 2, (lh + 1) // 2
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        peak_ops = 148 * 128 * sm_mhz * 1e6
+        prop_ms = fstages["prop"] if fstages else None
+        flow_res = {
+            "workload": f"{F} Driving pairs per GPU (left frames t, t+1), {P.levels} levels, r={P.patch_radius}, "
+                        f"{P.sweeps} sweeps/level, kNN {P.knn} on {P.desc_window}x{P.desc_window} WHT, "
+                        "forward + 2 inverse fields + consistency",
+            "ms_per_step": f_ms, "pairs_per_s": F * world / (f_ms * 1e-3),
+            "full_method_ms_per_step": full_ms,
+            "full_method_frames_per_s": F * world / (full_ms * 1e-3),
+            "stage_ms": fstages,
+            "valid_fraction": float(fval.mean()),
+            "epe_le_1px_on_valid": float((epe[fval] <= 1.0).mean()),
+            "roofline": None if not prop_ms else {
+                "bound": "alu", "kernel": "ff_prop_kernel", "achieved": ops / (prop_ms * 1e-3) / 1e12,
+                "peak": peak_ops / 1e12, "unit": "Tlane-op/s", "frac": ops / (prop_ms * 1e-3) / peak_ops,
+                "traffic": ncu_traffic("ff_prop_kernel"), "algorithmic_ops_per_call": ops,
+                "launch_ms_per_call": prop_ms,
+                "note": "row-sequential wavefront (left/up dependency): latency-bound, not issue-bound"},
+        }
+        ffh.close()
+        del sfo
+
     # ---------------- the evaluation step, timed on its own
     # (not part of the step above): KITTI outlier counts of the step's scene flow
     # against the generator's ground truth, one sgm_evaluate launch per step.
@@ -478,6 +555,7 @@ def main():
             "geometry": geo,
             "evaluate": evaluation,
             "stream": stream_res,
+            "flow": flow_res,
         }
         if gather:
             line["gather"] = gather
