@@ -253,6 +253,182 @@ __global__ void __launch_bounds__(128) ff_knn_kernel(const int32_t *__restrict__
         for (int k = 0; k < knn; ++k) nn[((long long)prob * n + qi) * knn + k] = bi[k];
 }
 
+// kNN on the tensor cores (window <= 8: |coefficient| <= 64 * 255 = 16320).  Every
+// coefficient splits exactly into signed 8-bit limbs c = 128 h + l (h in [-128, 127], l in
+// [0, 127]), so the query . database dot product is
+//   q.b = 16384 sum(qh bh) + 128 sum(qh bl + ql bh) + sum(ql bl),
+// three integer MMAs (mma.sync m16n8k32 s8 x s8 -> s32, exact) with the K = 32 operand
+// A = [qh | ql] and B = [bh | 0], [bl | bh], [0 | bl].  The epilogue forms the exact
+// distance |q|^2 + |b|^2 - 2 q.b in 64-bit integers and keeps a (distance, index)-ordered
+// top-k per query row; the 4 lanes holding a row merge their lists at the end.
+constexpr int kMmaTile = 64;             // database entries per shared-memory tile
+
+__device__ __forceinline__ void mma_s8(int (&c)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+    c[0] = c[1] = c[2] = c[3] = 0;
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// limbs of 4 consecutive coefficients packed as s8x4 (element 0 in the low byte)
+__device__ __forceinline__ void pack_limbs(const int32_t *c, unsigned &hw, unsigned &lw) {
+    hw = 0; lw = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        hw |= (unsigned(c[k] >> 7) & 0xffu) << (8 * k);
+        lw |= (unsigned(c[k] & 127)) << (8 * k);
+    }
+}
+
+// (distance, index)-ordered k-best list in local memory (insertions are rare once it has
+// filled); the caller keeps the admission threshold (k-th entry) in registers.
+struct KList {
+    long long d[kKnnMax];
+    int i[kKnnMax];
+};
+
+__device__ __forceinline__ void klist_init(KList &L) {
+    for (int k = 0; k < kKnnMax; ++k) { L.d[k] = 0x7fffffffffffffffll; L.i[k] = 0x7fffffff; }
+}
+
+// insert (dv, ci) and return the list's new k-th entry; the caller keeps the tighter of
+// that and any bound it already had (a bound shared from other lists stays valid)
+__device__ __noinline__ long long klist_insert(KList *L, long long dv, int ci, int knn, int *thr_i) {
+    bool ins = false;
+    for (int k = 0; k < knn; ++k) {
+        if (ins || dv < L->d[k] || (dv == L->d[k] && ci < L->i[k])) {
+            const long long td = L->d[k]; const int ti = L->i[k];
+            L->d[k] = dv; L->i[k] = ci; dv = td; ci = ti;
+            ins = true;
+        }
+    }
+    *thr_i = L->i[knn - 1];
+    return L->d[knn - 1];
+}
+
+#define KOFFER(L, thr, thr_i, dv, ci)                                          \
+    do {                                                                       \
+        const long long dv_ = (dv);                                            \
+        const int ci_ = (ci);                                                  \
+        if (dv_ < thr || (dv_ == thr && ci_ < thr_i)) {                        \
+            int ti_;                                                           \
+            const long long t_ = klist_insert(&L, dv_, ci_, knn, &ti_);       \
+            if (t_ < thr || (t_ == thr && ti_ < thr_i)) { thr = t_; thr_i = ti_; } \
+        }                                                                      \
+    } while (0)
+
+__global__ void __launch_bounds__(128) ff_knn_mma_kernel(const int32_t *__restrict__ desc, int n, int knn,
+                                                         int32_t *__restrict__ nn) {
+    __shared__ unsigned sBH[kMmaTile][4], sBL[kMmaTile][4];
+    __shared__ long long sBN[kMmaTile];
+    const int prob = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int32_t *dq = desc + (long long)prob * n * 16;
+    const int32_t *dd = desc + (long long)(prob ^ 1) * n * 16;
+    const int q0 = (blockIdx.x * 4 + warp) * 16;
+    const int r0 = q0 + g, r1 = q0 + g + 8;
+    unsigned a[4] = {0u, 0u, 0u, 0u};
+    long long qn0 = 0, qn1 = 0;
+    if (r0 < n) {
+        pack_limbs(dq + (long long)r0 * 16 + 4 * t, a[0], a[2]);
+        for (int k = 0; k < 4; ++k) { const long long c = dq[(long long)r0 * 16 + 4 * t + k]; qn0 += c * c; }
+    }
+    if (r1 < n) {
+        pack_limbs(dq + (long long)r1 * 16 + 4 * t, a[1], a[3]);
+        for (int k = 0; k < 4; ++k) { const long long c = dq[(long long)r1 * 16 + 4 * t + k]; qn1 += c * c; }
+    }
+    qn0 += __shfl_xor_sync(0xffffffffu, qn0, 1); qn0 += __shfl_xor_sync(0xffffffffu, qn0, 2);
+    qn1 += __shfl_xor_sync(0xffffffffu, qn1, 1); qn1 += __shfl_xor_sync(0xffffffffu, qn1, 2);
+    KList L0, L1;
+    klist_init(L0);
+    klist_init(L1);
+    long long thr0 = r0 < n ? 0x7fffffffffffffffll : -1ll, thr1 = r1 < n ? 0x7fffffffffffffffll : -1ll;
+    int thr0_i = 0x7fffffff, thr1_i = 0x7fffffff;
+    const int ntiles = (n + kMmaTile - 1) / kMmaTile;
+    const int tq = min(int((long long)blockIdx.x * 64 / kMmaTile), ntiles - 1);
+    for (int it = 0; it < ntiles; ++it) {
+        const int up = ntiles - 1 - tq, dn = tq;
+        const int h = (it + 1) / 2;
+        int tt;
+        if (it == 0) tt = tq;
+        else if (h <= min(up, dn)) tt = (it & 1) ? tq + h : tq - h;
+        else tt = up > dn ? tq + (it - dn) : tq - (it - up);
+        const int base = tt * kMmaTile;
+        __syncthreads();
+        if (threadIdx.x < kMmaTile) {
+            const int e = base + threadIdx.x;
+            long long bn = 0;
+            if (e < n) {
+                const int32_t *c = dd + (long long)e * 16;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) pack_limbs(c + 4 * w, sBH[threadIdx.x][w], sBL[threadIdx.x][w]);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) bn += (long long)c[k] * c[k];
+            } else {
+#pragma unroll
+                for (int w = 0; w < 4; ++w) { sBH[threadIdx.x][w] = 0u; sBL[threadIdx.x][w] = 0u; }
+            }
+            sBN[threadIdx.x] = bn;
+        }
+        __syncthreads();
+        // Each lane sees 2 of every 8 columns; the row's final k-th best is at most the
+        // smallest of the 4 lanes' k-th best, so every lane may use that (a pair compared
+        // lexicographically) as its admission bound.
+#pragma unroll
+        for (int m = 1; m <= 2; m <<= 1) {
+            const long long o0 = __shfl_xor_sync(0xffffffffu, thr0, m);
+            const int oi0 = __shfl_xor_sync(0xffffffffu, thr0_i, m);
+            const long long o1 = __shfl_xor_sync(0xffffffffu, thr1, m);
+            const int oi1 = __shfl_xor_sync(0xffffffffu, thr1_i, m);
+            if (o0 < thr0 || (o0 == thr0 && oi0 < thr0_i)) { thr0 = o0; thr0_i = oi0; }
+            if (o1 < thr1 || (o1 == thr1 && oi1 < thr1_i)) { thr1 = o1; thr1_i = oi1; }
+        }
+        for (int cg = 0; cg < kMmaTile / 8; ++cg) {
+            const unsigned bh = sBH[cg * 8 + g][t], bl = sBL[cg * 8 + g][t];
+            int c1[4], c2[4], c3[4];
+            mma_s8(c1, a, bh, 0u);
+            mma_s8(c2, a, bl, bh);
+            mma_s8(c3, a, 0u, bl);
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+                const int col = cg * 8 + 2 * t + jj;
+                const int idx = base + col;
+                if (idx < n) {
+                    const long long bn = sBN[col];
+                    const long long dot0 = 16384ll * c1[jj] + 128ll * c2[jj] + c3[jj];
+                    const long long dot1 = 16384ll * c1[2 + jj] + 128ll * c2[2 + jj] + c3[2 + jj];
+                    KOFFER(L0, thr0, thr0_i, qn0 + bn - 2 * dot0, idx);
+                    KOFFER(L1, thr1, thr1_i, qn1 + bn - 2 * dot1, idx);
+                }
+            }
+        }
+    }
+    // merge the 4 partial lists of each row into lane t = 0, admitting against lane 0's own
+    // list (the shared bound may equal another lane's k-th entry, which must be merged)
+    thr0 = L0.d[knn - 1]; thr0_i = L0.i[knn - 1];
+    thr1 = L1.d[knn - 1]; thr1_i = L1.i[knn - 1];
+    for (int src = 1; src < 4; ++src) {
+        for (int k = 0; k < knn; ++k) {
+            const long long d0 = __shfl_sync(0xffffffffu, L0.d[k], (lane & ~3) | src);
+            const int i0 = __shfl_sync(0xffffffffu, L0.i[k], (lane & ~3) | src);
+            const long long d1 = __shfl_sync(0xffffffffu, L1.d[k], (lane & ~3) | src);
+            const int i1 = __shfl_sync(0xffffffffu, L1.i[k], (lane & ~3) | src);
+            if (t == 0) {
+                if (i0 != 0x7fffffff) KOFFER(L0, thr0, thr0_i, d0, i0);
+                if (i1 != 0x7fffffff) KOFFER(L1, thr1, thr1_i, d1, i1);
+            }
+        }
+    }
+    if (t == 0) {
+        if (r0 < n)
+            for (int k = 0; k < knn; ++k) nn[((long long)prob * n + r0) * knn + k] = L0.i[k];
+        if (r1 < n)
+            for (int k = 0; k < knn; ++k) nn[((long long)prob * n + r1) * knn + k] = L1.i[k];
+    }
+}
+
 // ------------------------------------------------------------------ fields
 // A field f of a batch: pair k = f / fpp, kind = f % fpp; kind 0 matches A_k -> B_k,
 // kinds 1, 2 match B_k -> A_k (the two inverse fields, F-5).
@@ -593,10 +769,15 @@ cudaError_t ff_launch_wht(const uint8_t *img, long long img_stride, int W, int H
     return cudaGetLastError();
 }
 
-cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int32_t *nn, cudaStream_t st) {
+cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int win, int32_t *nn, cudaStream_t st) {
     if (knn < 1 || knn > kKnnMax) return cudaErrorInvalidValue;
-    dim3 grid((n + 127) / 128, nprob);
-    ff_knn_kernel<<<grid, 128, 0, st>>>(desc, n, knn, nn);
+    if (win <= 8) {                         // coefficients fit two s8 limbs: tensor cores
+        dim3 grid((n + 63) / 64, nprob);
+        ff_knn_mma_kernel<<<grid, 128, 0, st>>>(desc, n, knn, nn);
+    } else {
+        dim3 grid((n + 127) / 128, nprob);
+        ff_knn_kernel<<<grid, 128, 0, st>>>(desc, n, knn, nn);
+    }
     return cudaGetLastError();
 }
 

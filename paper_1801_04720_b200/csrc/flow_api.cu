@@ -116,7 +116,7 @@ cudaError_t run_fields(sgm_flow_handle *h, int n, int fpp, uint64_t seed, int ra
     if (e != cudaSuccess) return e;
     ++h->launches;
     T.begin(2);
-    e = sgm::ff_launch_knn(h->desc, int(h->lper[c]), 2 * n, P.knn, h->nn, st);
+    e = sgm::ff_launch_knn(h->desc, int(h->lper[c]), 2 * n, P.knn, P.desc_window, h->nn, st);
     T.end();
     if (e != cudaSuccess) return e;
     ++h->launches;
@@ -276,7 +276,7 @@ sgm_status sgm_flow_knn_init(sgm_flow_handle *h, const uint8_t *A, const uint8_t
     if (e == cudaSuccess) e = cudaMemcpyAsync(h->pyr + h->pyr_img, B, size_t(n), cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess) e = sgm::ff_launch_quad(h->pyr, h->pyr_img, w, hgt, 2, h->quad, h->pyr_img, st);
     if (e == cudaSuccess) e = sgm::ff_launch_wht(h->pyr, h->pyr_img, w, hgt, h->prm.desc_window, 2, h->desc, st);
-    if (e == cudaSuccess) e = sgm::ff_launch_knn(h->desc, int(n), 1, h->prm.knn, nn ? nn : h->nn, st);
+    if (e == cudaSuccess) e = sgm::ff_launch_knn(h->desc, int(n), 1, h->prm.knn, h->prm.desc_window, nn ? nn : h->nn, st);
     sgm::FFFields F{};
     F.W = w; F.H = hgt; F.fpp = 1; F.nfields = 1;
     F.A = h->pyr; F.B = h->pyr + h->pyr_img; F.img_stride = 2 * h->pyr_img;
