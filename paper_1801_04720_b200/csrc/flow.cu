@@ -24,6 +24,8 @@
 //   ff_search_kernel      the random search after each sweep (thread per pixel, counter RNG)
 //   ff_lift_kernel        x2 vectors, nearest-neighbour upsampling, costs recomputed
 //   ff_consistency_kernel two-inverse-field check (thread per pixel)
+#include <cuda_fp16.h>
+
 #include "sgm_internal.cuh"
 
 namespace sgm {
@@ -254,33 +256,14 @@ __global__ void __launch_bounds__(128) ff_knn_kernel(const int32_t *__restrict__
 }
 
 // kNN on the tensor cores (window <= 8: |coefficient| <= 64 * 255 = 16320).  Every
-// coefficient splits exactly into signed 8-bit limbs c = 128 h + l (h in [-128, 127], l in
-// [0, 127]), so the query . database dot product is
+// coefficient splits exactly into limbs c = 128 h + l (h in [-128, 127], l in [0, 127]),
+// so the query . database dot product is
 //   q.b = 16384 sum(qh bh) + 128 sum(qh bl + ql bh) + sum(ql bl),
-// three integer MMAs (mma.sync m16n8k32 s8 x s8 -> s32, exact) with the K = 32 operand
-// A = [qh | ql] and B = [bh | 0], [bl | bh], [0 | bl].  The epilogue forms the exact
-// distance |q|^2 + |b|^2 - 2 q.b in 64-bit integers and keeps a (distance, index)-ordered
-// top-k per query row; the 4 lanes holding a row merge their lists at the end.
+// four m16n8k16 MMAs per 16 x 8 tile.  The epilogue forms the exact distance
+// |q|^2 + |b|^2 - 2 q.b in 64-bit integers where needed and keeps a (distance,
+// index)-ordered top-k per query row; the 4 lanes holding a row merge their lists at the
+// end.
 constexpr int kMmaTile = 64;             // database entries per shared-memory tile
-
-__device__ __forceinline__ void mma_s8(int (&c)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
-    c[0] = c[1] = c[2] = c[3] = 0;
-    asm volatile(
-        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};\n"
-        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-// limbs of 4 consecutive coefficients packed as s8x4 (element 0 in the low byte)
-__device__ __forceinline__ void pack_limbs(const int32_t *c, unsigned &hw, unsigned &lw) {
-    hw = 0; lw = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        hw |= (unsigned(c[k] >> 7) & 0xffu) << (8 * k);
-        lw |= (unsigned(c[k] & 127)) << (8 * k);
-    }
-}
 
 // (distance, index)-ordered k-best list in local memory (insertions are rare once it has
 // filled); the caller keeps the admission threshold (k-th entry) in registers.
@@ -319,63 +302,127 @@ __device__ __noinline__ long long klist_insert(KList *L, long long dv, int ci, i
         }                                                                      \
     } while (0)
 
-__global__ void __launch_bounds__(128) ff_knn_mma_kernel(const int32_t *__restrict__ desc, int n, int knn,
-                                                         int32_t *__restrict__ nn) {
-    __shared__ unsigned sBH[kMmaTile][4], sBL[kMmaTile][4];
-    __shared__ long long sBN[kMmaTile];
+// fp16 variant of the same exact decomposition: the limbs (|h| <= 128, l <= 127) are exact
+// fp16 values, every product is < 2^14 and every partial sum of 16 or 32 of them < 2^24,
+// so the fp32 accumulators hold the exact integers.  The epilogue first rejects in fp32
+// (error < 2^13 against a 2^15 margin) and forms the exact 64-bit distance only for the
+// rare entries within the margin of the admission bound.
+__device__ __forceinline__ void mma_f16(float (&c)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ unsigned half2_bits(int lo, int hi) {
+    const __half2 v = __floats2half2_rn(float(lo), float(hi));
+    return *reinterpret_cast<const unsigned *>(&v);
+}
+
+// Packed database entry (64 B + norms): limbs of the 16 coefficients as half2 words,
+// word w = dims (2w, 2w+1); computed once per image by ff_knn_prep_kernel.
+struct KnnEntry {
+    unsigned bh[8], bl[8];
+};
+
+// norms are stored per problem with a stride n_pad = n rounded up to 4 (16-byte aligned
+// rows for cp.async)
+__global__ void ff_knn_prep_kernel(const int32_t *__restrict__ desc, int n, int n_pad, long long total,
+                                   KnnEntry *__restrict__ ent, long long *__restrict__ norm,
+                                   float *__restrict__ normf) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long pe = (e / n) * n_pad + e % n;
+        const int32_t *c = desc + e * 16;
+        KnnEntry k;
+        long long bn = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            k.bh[w] = half2_bits(c[2 * w] >> 7, c[2 * w + 1] >> 7);
+            k.bl[w] = half2_bits(c[2 * w] & 127, c[2 * w + 1] & 127);
+            bn += (long long)c[2 * w] * c[2 * w] + (long long)c[2 * w + 1] * c[2 * w + 1];
+        }
+        ent[e] = k;
+        norm[pe] = bn;
+        normf[pe] = float(bn);
+    }
+}
+
+__device__ __forceinline__ void cp_async16_ff(void *smem, const void *gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__global__ void __launch_bounds__(128) ff_knn_mma_kernel(const KnnEntry *__restrict__ ent,
+                                                         const long long *__restrict__ norm,
+                                                         const float *__restrict__ normf, int n, int n_pad,
+                                                         int knn, int32_t *__restrict__ nn) {
+    __shared__ __align__(16) KnnEntry sE[2][kMmaTile];
+    __shared__ __align__(16) long long sN[2][kMmaTile];
+    __shared__ __align__(16) float sNf[2][kMmaTile];
     const int prob = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int32_t *dq = desc + (long long)prob * n * 16;
-    const int32_t *dd = desc + (long long)(prob ^ 1) * n * 16;
+    const KnnEntry *eq = ent + (long long)prob * n;
+    const KnnEntry *ed = ent + (long long)(prob ^ 1) * n;
+    const long long *nq = norm + (long long)prob * n_pad, *nd = norm + (long long)(prob ^ 1) * n_pad;
+    const float *nfd = normf + (long long)(prob ^ 1) * n_pad;
     const int q0 = (blockIdx.x * 4 + warp) * 16;
     const int r0 = q0 + g, r1 = q0 + g + 8;
-    unsigned a[4] = {0u, 0u, 0u, 0u};
-    long long qn0 = 0, qn1 = 0;
-    if (r0 < n) {
-        pack_limbs(dq + (long long)r0 * 16 + 4 * t, a[0], a[2]);
-        for (int k = 0; k < 4; ++k) { const long long c = dq[(long long)r0 * 16 + 4 * t + k]; qn0 += c * c; }
-    }
-    if (r1 < n) {
-        pack_limbs(dq + (long long)r1 * 16 + 4 * t, a[1], a[3]);
-        for (int k = 0; k < 4; ++k) { const long long c = dq[(long long)r1 * 16 + 4 * t + k]; qn1 += c * c; }
-    }
-    qn0 += __shfl_xor_sync(0xffffffffu, qn0, 1); qn0 += __shfl_xor_sync(0xffffffffu, qn0, 2);
-    qn1 += __shfl_xor_sync(0xffffffffu, qn1, 1); qn1 += __shfl_xor_sync(0xffffffffu, qn1, 2);
+    // A fragments (m16n8k16, row-major 16 x 16): a0 = row g, k 2t..2t+1; a1 = row g+8;
+    // a2 = row g, k 2t+8..2t+9; a3 = row g+8, k 2t+8..2t+9
+    unsigned ah[4] = {0u, 0u, 0u, 0u}, al[4] = {0u, 0u, 0u, 0u};
+    if (r0 < n) { ah[0] = eq[r0].bh[t]; ah[2] = eq[r0].bh[t + 4]; al[0] = eq[r0].bl[t]; al[2] = eq[r0].bl[t + 4]; }
+    if (r1 < n) { ah[1] = eq[r1].bh[t]; ah[3] = eq[r1].bh[t + 4]; al[1] = eq[r1].bl[t]; al[3] = eq[r1].bl[t + 4]; }
+    const long long qn0 = r0 < n ? nq[r0] : 0, qn1 = r1 < n ? nq[r1] : 0;
     KList L0, L1;
     klist_init(L0);
     klist_init(L1);
     long long thr0 = r0 < n ? 0x7fffffffffffffffll : -1ll, thr1 = r1 < n ? 0x7fffffffffffffffll : -1ll;
     int thr0_i = 0x7fffffff, thr1_i = 0x7fffffff;
+    const float kMargin = 32768.f;
+    const float qn0f = float(qn0), qn1f = float(qn1);
     const int ntiles = (n + kMmaTile - 1) / kMmaTile;
     const int tq = min(int((long long)blockIdx.x * 64 / kMmaTile), ntiles - 1);
-    for (int it = 0; it < ntiles; ++it) {
+    auto tile_of = [&](int it) {
         const int up = ntiles - 1 - tq, dn = tq;
         const int h = (it + 1) / 2;
-        int tt;
-        if (it == 0) tt = tq;
-        else if (h <= min(up, dn)) tt = (it & 1) ? tq + h : tq - h;
-        else tt = up > dn ? tq + (it - dn) : tq - (it - up);
-        const int base = tt * kMmaTile;
-        __syncthreads();
-        if (threadIdx.x < kMmaTile) {
-            const int e = base + threadIdx.x;
-            long long bn = 0;
-            if (e < n) {
-                const int32_t *c = dd + (long long)e * 16;
-#pragma unroll
-                for (int w = 0; w < 4; ++w) pack_limbs(c + 4 * w, sBH[threadIdx.x][w], sBL[threadIdx.x][w]);
-#pragma unroll
-                for (int k = 0; k < 16; ++k) bn += (long long)c[k] * c[k];
-            } else {
-#pragma unroll
-                for (int w = 0; w < 4; ++w) { sBH[threadIdx.x][w] = 0u; sBL[threadIdx.x][w] = 0u; }
-            }
-            sBN[threadIdx.x] = bn;
+        if (it == 0) return tq;
+        if (h <= min(up, dn)) return (it & 1) ? tq + h : tq - h;
+        return up > dn ? tq + (it - dn) : tq - (it - up);
+    };
+    // cp.async one tile (64 entries x 64 B + norms) into buffer b; entries past n are not
+    // loaded (their columns are skipped by idx < n)
+    auto load_tile = [&](int it, int b) {
+        const int base = tile_of(it) * kMmaTile;
+        for (int u = threadIdx.x; u < kMmaTile * 4; u += blockDim.x) {        // 4 x 16 B per entry
+            const int e = u >> 2, part = u & 3;
+            if (base + e < n) cp_async16_ff(reinterpret_cast<char *>(&sE[b][e]) + 16 * part,
+                                            reinterpret_cast<const char *>(ed + base + e) + 16 * part);
+        }
+        for (int u = threadIdx.x; u < kMmaTile / 2; u += blockDim.x)          // norms: 2 per 16 B
+            if (base + 2 * u + 1 < n) cp_async16_ff(&sN[b][2 * u], nd + base + 2 * u);
+            else if (base + 2 * u < n) sN[b][2 * u] = nd[base + 2 * u];
+        for (int u = threadIdx.x; u < kMmaTile / 4; u += blockDim.x)          // fp32 norms: 4 per 16 B
+            if (base + 4 * u + 3 < n) cp_async16_ff(&sNf[b][4 * u], nfd + base + 4 * u);
+            else
+                for (int k = 0; k < 4; ++k)
+                    if (base + 4 * u + k < n) sNf[b][4 * u + k] = nfd[base + 4 * u + k];
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    load_tile(0, 0);
+    for (int it = 0; it < ntiles; ++it) {
+        const int b = it & 1;
+        if (it + 1 < ntiles) {
+            load_tile(it + 1, b ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         __syncthreads();
-        // Each lane sees 2 of every 8 columns; the row's final k-th best is at most the
-        // smallest of the 4 lanes' k-th best, so every lane may use that (a pair compared
-        // lexicographically) as its admission bound.
+        const int base = tile_of(it) * kMmaTile;
+        // shared admission bound of the row: each lane sees 2 of every 8 columns; the
+        // row's final k-th best is at most the smallest of the 4 lanes' k-th best
 #pragma unroll
         for (int m = 1; m <= 2; m <<= 1) {
             const long long o0 = __shfl_xor_sync(0xffffffffu, thr0, m);
@@ -385,25 +432,41 @@ __global__ void __launch_bounds__(128) ff_knn_mma_kernel(const int32_t *__restri
             if (o0 < thr0 || (o0 == thr0 && oi0 < thr0_i)) { thr0 = o0; thr0_i = oi0; }
             if (o1 < thr1 || (o1 == thr1 && oi1 < thr1_i)) { thr1 = o1; thr1_i = oi1; }
         }
+        float lim0 = float(thr0) + kMargin, lim1 = float(thr1) + kMargin;
         for (int cg = 0; cg < kMmaTile / 8; ++cg) {
-            const unsigned bh = sBH[cg * 8 + g][t], bl = sBL[cg * 8 + g][t];
-            int c1[4], c2[4], c3[4];
-            mma_s8(c1, a, bh, 0u);
-            mma_s8(c2, a, bl, bh);
-            mma_s8(c3, a, 0u, bl);
+            // B fragment (16 x 8, col): b0 = k 2t..2t+1, b1 = k 2t+8..2t+9 of column g
+            const KnnEntry &E = sE[b][cg * 8 + g];
+            const unsigned bh0 = E.bh[t], bh1 = E.bh[t + 4], bl0 = E.bl[t], bl1 = E.bl[t + 4];
+            float c1[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f}, c3[4] = {0.f, 0.f, 0.f, 0.f};
+            mma_f16(c1, ah, bh0, bh1);              // sum qh bh
+            mma_f16(c2, ah, bl0, bl1);              // + sum qh bl
+            mma_f16(c2, al, bh0, bh1);              // + sum ql bh
+            mma_f16(c3, al, bl0, bl1);              // sum ql bl
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) {
                 const int col = cg * 8 + 2 * t + jj;
                 const int idx = base + col;
-                if (idx < n) {
-                    const long long bn = sBN[col];
-                    const long long dot0 = 16384ll * c1[jj] + 128ll * c2[jj] + c3[jj];
-                    const long long dot1 = 16384ll * c1[2 + jj] + 128ll * c2[2 + jj] + c3[2 + jj];
-                    KOFFER(L0, thr0, thr0_i, qn0 + bn - 2 * dot0, idx);
-                    KOFFER(L1, thr1, thr1_i, qn1 + bn - 2 * dot1, idx);
+                const float bnf = sNf[b][col];
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const float dotf = fmaf(16384.f, c1[2 * rr + jj], fmaf(128.f, c2[2 * rr + jj], c3[2 * rr + jj]));
+                    const float df = fmaf(-2.f, dotf, (rr ? qn1f : qn0f) + bnf);
+                    if (df <= (rr ? lim1 : lim0) && idx < n) {
+                        const long long dot = 16384ll * (long long)c1[2 * rr + jj] +
+                                              128ll * (long long)c2[2 * rr + jj] + (long long)c3[2 * rr + jj];
+                        const long long d = (rr ? qn1 : qn0) + sN[b][col] - 2 * dot;
+                        if (rr) {
+                            KOFFER(L1, thr1, thr1_i, d, idx);
+                            lim1 = float(thr1) + kMargin;
+                        } else {
+                            KOFFER(L0, thr0, thr0_i, d, idx);
+                            lim0 = float(thr0) + kMargin;
+                        }
+                    }
                 }
             }
         }
+        __syncthreads();                             // buffer b is refilled next iteration
     }
     // merge the 4 partial lists of each row into lane t = 0, admitting against lane 0's own
     // list (the shared bound may equal another lane's k-th entry, which must be merged)
@@ -769,11 +832,25 @@ cudaError_t ff_launch_wht(const uint8_t *img, long long img_stride, int W, int H
     return cudaGetLastError();
 }
 
-cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int win, int32_t *nn, cudaStream_t st) {
+size_t ff_knn_scratch_bytes(long long entries) {
+    // entries + norms with per-problem padding (<= 3 per problem; nprob <= entries)
+    return size_t(entries) * sizeof(KnnEntry) + size_t(entries) * 4 * (sizeof(long long) + sizeof(float)) + 256;
+}
+
+cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int win, int32_t *nn, void *scratch,
+                          cudaStream_t st) {
     if (knn < 1 || knn > kKnnMax) return cudaErrorInvalidValue;
-    if (win <= 8) {                         // coefficients fit two s8 limbs: tensor cores
+    if (win <= 8) {                         // coefficients fit two exact limbs: tensor cores
+        // every problem's query image and its partner database image (nprob may be odd: one
+        // problem of a pair)
+        const long long total = (long long)n * (nprob + (nprob & 1));
+        const int n_pad = (n + 3) & ~3;
+        KnnEntry *ent = reinterpret_cast<KnnEntry *>(scratch);
+        long long *norm = reinterpret_cast<long long *>(ent + total);
+        float *normf = reinterpret_cast<float *>(norm + (long long)n_pad * (nprob + (nprob & 1)));
+        ff_knn_prep_kernel<<<ff_grid(total, 128), 128, 0, st>>>(desc, n, n_pad, total, ent, norm, normf);
         dim3 grid((n + 63) / 64, nprob);
-        ff_knn_mma_kernel<<<grid, 128, 0, st>>>(desc, n, knn, nn);
+        ff_knn_mma_kernel<<<grid, 128, 0, st>>>(ent, norm, normf, n, n_pad, knn, nn);
     } else {
         dim3 grid((n + 127) / 128, nprob);
         ff_knn_kernel<<<grid, 128, 0, st>>>(desc, n, knn, nn);

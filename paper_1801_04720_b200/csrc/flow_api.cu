@@ -17,6 +17,7 @@ struct sgm_flow_handle {
     uint32_t *quad = nullptr;        // [max_batch][2][pyr_img]: their quad images (same offsets)
     int32_t *desc = nullptr;         // [2 max_batch][Wc Hc][16]
     int32_t *nn = nullptr;           // [2 max_batch][Wc Hc][knn]
+    void *knn_scratch = nullptr;     // packed descriptors for the tensor-core kNN
     int32_t *flow[2] = {nullptr, nullptr};   // ping-pong [3 max_batch][W H][2]
     int32_t *cost[2] = {nullptr, nullptr};   // [3 max_batch][W H]
     int *sync = nullptr;             // ticket + band progress of the propagation kernel
@@ -48,7 +49,7 @@ cudaError_t ff_alloc(T **p, size_t count) {
 }
 
 void ff_free(sgm_flow_handle *h) {
-    void *ptrs[] = {h->pyr, h->quad, h->desc, h->nn, h->flow[0], h->flow[1], h->cost[0], h->cost[1], h->sync};
+    void *ptrs[] = {h->knn_scratch, h->pyr, h->quad, h->desc, h->nn, h->flow[0], h->flow[1], h->cost[0], h->cost[1], h->sync};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (auto &e : h->ev)
@@ -116,7 +117,7 @@ cudaError_t run_fields(sgm_flow_handle *h, int n, int fpp, uint64_t seed, int ra
     if (e != cudaSuccess) return e;
     ++h->launches;
     T.begin(2);
-    e = sgm::ff_launch_knn(h->desc, int(h->lper[c]), 2 * n, P.knn, P.desc_window, h->nn, st);
+    e = sgm::ff_launch_knn(h->desc, int(h->lper[c]), 2 * n, P.knn, P.desc_window, h->nn, h->knn_scratch, st);
     T.end();
     if (e != cudaSuccess) return e;
     ++h->launches;
@@ -188,8 +189,12 @@ sgm_status sgm_flow_create(const sgm_flow_params *p, int32_t device, sgm_flow_ha
     const size_t n0 = size_t(h->lper[0]), nc = size_t(h->lper[p->levels - 1]);
     if (e == cudaSuccess) e = ff_alloc(&h->pyr, mb * 2 * size_t(h->pyr_img));
     if (e == cudaSuccess) e = ff_alloc(&h->quad, mb * 2 * size_t(h->pyr_img));
-    if (e == cudaSuccess) e = ff_alloc(&h->desc, 2 * mb * nc * 16);
-    if (e == cudaSuccess) e = ff_alloc(&h->nn, 2 * mb * nc * size_t(p->knn));
+    // descriptors / neighbour lists: the batch at the coarsest level, or one pair at level 0
+    // (the stage-wise sgm_flow_knn_init)
+    const size_t nd = 2 * mb * nc > 2 * n0 ? 2 * mb * nc : 2 * n0;
+    if (e == cudaSuccess) e = ff_alloc(&h->desc, nd * 16);
+    if (e == cudaSuccess) e = ff_alloc(&h->nn, nd * size_t(p->knn));
+    if (e == cudaSuccess) e = cudaMalloc(&h->knn_scratch, sgm::ff_knn_scratch_bytes((long long)nd));
     for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
         e = ff_alloc(&h->flow[k], 3 * mb * n0 * 2);
         if (e == cudaSuccess) e = ff_alloc(&h->cost[k], 3 * mb * n0);
@@ -276,7 +281,7 @@ sgm_status sgm_flow_knn_init(sgm_flow_handle *h, const uint8_t *A, const uint8_t
     if (e == cudaSuccess) e = cudaMemcpyAsync(h->pyr + h->pyr_img, B, size_t(n), cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess) e = sgm::ff_launch_quad(h->pyr, h->pyr_img, w, hgt, 2, h->quad, h->pyr_img, st);
     if (e == cudaSuccess) e = sgm::ff_launch_wht(h->pyr, h->pyr_img, w, hgt, h->prm.desc_window, 2, h->desc, st);
-    if (e == cudaSuccess) e = sgm::ff_launch_knn(h->desc, int(n), 1, h->prm.knn, h->prm.desc_window, nn ? nn : h->nn, st);
+    if (e == cudaSuccess) e = sgm::ff_launch_knn(h->desc, int(n), 1, h->prm.knn, h->prm.desc_window, nn ? nn : h->nn, h->knn_scratch, st);
     sgm::FFFields F{};
     F.W = w; F.H = hgt; F.fpp = 1; F.nfields = 1;
     F.A = h->pyr; F.B = h->pyr + h->pyr_img; F.img_stride = 2 * h->pyr_img;

@@ -114,7 +114,9 @@ cudaError_t ff_launch_downsample(const uint8_t *src, long long src_stride, int W
                                  long long dst_stride, int nimg, cudaStream_t st);
 cudaError_t ff_launch_wht(const uint8_t *img, long long img_stride, int W, int H, int win, int nimg,
                           int32_t *desc, cudaStream_t st);
-cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int win, int32_t *nn, cudaStream_t st);
+cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int win, int32_t *nn, void *scratch,
+                          cudaStream_t st);
+size_t ff_knn_scratch_bytes(long long entries);
 cudaError_t ff_launch_init(const FFFields &F, const int32_t *nn, int knn, cudaStream_t st);
 cudaError_t ff_launch_lift(const FFFields &F, const int32_t *coarse, int Wc, int Hc, cudaStream_t st);
 // stage timer of the flow handle (flow_api.cu): begin(category) / end() around a launch
