@@ -664,6 +664,8 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
 #pragma unroll
     for (int k = 0; k < NK; ++k) aoff[k] = (long long)clampi(y + sdy[k], 0, H - 1) * W;
     int2 hv = make_int2(0, 0);                      // vector of the previous pixel in scan order
+    unsigned long long hbuf = 0ull;                 // band handoff entries hbase + lane
+    int hbase = 0;
     // incumbent of the next position, loaded one position ahead
     int nx0 = fwd ? 0 : W - 1;
     long long np = (long long)y * W + nx0;
@@ -676,10 +678,6 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
             np = p + (fwd ? 1 : -1);
             ncu = flow[2 * np]; ncv = flow[2 * np + 1]; ncc = cost[np];
         }
-        int a[NK];
-#pragma unroll
-        for (int k = 0; k < NK; ++k)
-            a[k] = __ldg(src + aoff[k] + clampi(x + sdx[k], 0, W - 1));
         // vertical candidate: the finished vector of (x, row above in scan order)
         int2 vv = make_int2(0, 0);
         if (has_above) {
@@ -689,7 +687,18 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
                 // warps that have work
                 while (hand_tag(e = ring_in[i & (kRowRing - 1)]) != i + 1) __nanosleep(20);
             } else {
-                while (hand_tag(e = ld_relaxed_u64(hin + i)) != i + 1) __nanosleep(32);
+                // band handoff through L2: fetch 32 positions per round trip (lane l holds
+                // position hbase + l) and re-poll only when the producer is not there yet
+                if ((i & 31) == 0) {
+                    hbase = i;
+                    hbuf = hbase + lane < W ? ld_relaxed_u64(hin + hbase + lane) : 0ull;
+                }
+                e = __shfl_sync(0xffffffffu, hbuf, i & 31);
+                while (hand_tag(e) != i + 1) {
+                    __nanosleep(64);
+                    hbuf = hbase + lane < W ? ld_relaxed_u64(hin + hbase + lane) : 0ull;
+                    e = __shfl_sync(0xffffffffu, hbuf, i & 31);
+                }
             }
             vv = hand_vec(e);
         }
@@ -697,6 +706,12 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
         // the incumbent (their data term equals the incumbent's: never strictly better)
         const bool eh = i > 0 && (hv.x != cu || hv.y != cv);
         const bool ev = has_above && (vv.x != cu || vv.y != cv) && (!eh || vv.x != hv.x || vv.y != hv.y);
+        int a[NK];                                  // A samples, loaded only when needed
+        if (eh || ev) {
+#pragma unroll
+            for (int k = 0; k < NK; ++k)
+                a[k] = __ldg(src + aoff[k] + clampi(x + sdx[k], 0, W - 1));
+        }
         if (eh && ev) {                             // both candidates: loads in flight together
             const Cand C0(hv.x, hv.y, W, H), C1(vv.x, vv.y, W, H);
             int s0 = 0, s1 = 0;
