@@ -70,6 +70,10 @@ def _get():
             lib.orc_ff_field.argtypes = [P, P, I, I, I, I, I, I, I, I, I, U64, P, P]
             lib.orc_ff_consistency.argtypes = [P, P, P, I, I, I, P]
             lib.orc_ff_flow.argtypes = [P, P, I, I, I, I, I, I, I, I, I, U64, I, P, P]
+            lib.orc_edge_distance.argtypes = [P, I, I, I, I, I, I, Dd]
+            lib.orc_edge_distance.restype = Dd
+            lib.orc_densify.argtypes = [P, P, P, I, I, I, I, Dd, P]
+            lib.orc_densify.restype = ctypes.c_int
             for fn in ("orc_ff_downsample", "orc_ff_wht", "orc_ff_knn_init", "orc_ff_sweep",
                        "orc_ff_lift", "orc_ff_field", "orc_ff_consistency", "orc_ff_flow"):
                 getattr(lib, fn).restype = ctypes.c_int
@@ -395,3 +399,28 @@ def ff_flow(A, B, levels=3, r=4, sweeps=8, R0=8, win=8, knn=4, penalty=20, seed=
     _chk(_get().orc_ff_flow(_p(A), _p(B), W, H, levels, r, sweeps, R0, win, knn, penalty, seed,
                             thr_q, _p(flow), _p(v)), "ff_flow")
     return flow, v
+
+
+# ---------------------------------------------------------------- densification (flow_oracle.c)
+def edge_distance(guide, p, s, lam=1.0):
+    guide = _c(guide, np.uint8)
+    H, W = guide.shape
+    return float(_get().orc_edge_distance(_p(guide), W, H, p[0], p[1], s[0], s[1], lam))
+
+
+def densify(field, valid, guide, K=25, lam=1.0):
+    """Fill the gaps of a C-channel field [H][W][C] (C <= 4): each gap pixel takes the
+    1/d_e-weighted mean of its K nearest valid seeds.  Returns float64 [H][W][C]; raises
+    if the image has no valid pixel (SPEC S:258 error)."""
+    field = _c(field, np.float32)
+    if field.ndim == 2:
+        field = field[..., None]
+    valid = _c(valid, np.uint8)
+    guide = _c(guide, np.uint8)
+    H, W, C = field.shape
+    out = np.empty((H, W, C), np.float64)
+    rc = _get().orc_densify(_p(field), _p(valid), _p(guide), W, H, C, K, lam, _p(out))
+    if rc == 3:
+        raise ValueError("densify: no valid pixel")
+    _chk(rc, "densify")
+    return out
