@@ -69,6 +69,22 @@ SGM_API sgm_status sgm_flow(sgm_flow_handle *h, int32_t n, const uint8_t *frames
                     const uint8_t *frames1, float *flow, uint8_t *valid, int32_t *fields_q,
                     void *stream);
 
+/* ---- densification ------------------------------- */
+/* Edge-aware gap filling of a sparse field (SPEC densify S:253-262, F-6; the gap filling the
+ * paper delegates to EpicFlow, and the "Ours (All)" densification):
+ * a pixel with valid != 0 keeps its values exactly; a gap pixel p takes the mean of its K
+ * nearest valid seeds s (squared Euclidean distance, ties to the smaller linear index)
+ * weighted by 1 / (|p - s| + lambda * sum_k g(q_k)), q_k the interior points of the
+ * segment p -> s (n = max(|dx|,|dy|) steps, rounded half up) and g the guide's L1
+ * central-difference gradient (readings DN1-DN4).  No handle: plain device pointers.
+ *   field, out [n][H][W][C] float32 (C = 1..4: flow (u, v), scene flow (u, v, d0, d1), ...);
+ *   valid, guide [n][H][W] uint8; 1 <= K <= 64; lambda >= 0 (gray levels -> px, 1.0);
+ *   unfilled (device int32, nullable): number of pixels of images without any valid pixel
+ *   (their output is 0, the SPEC's "zero valid pixels" error).  Arithmetic in float32. */
+SGM_API sgm_status sgm_densify(int32_t n, int32_t width, int32_t height, int32_t channels,
+                       const float *field, const uint8_t *valid, const uint8_t *guide,
+                       int32_t K, float lambda, float *out, int32_t *unfilled, void *stream);
+
 /* ---- instrumentation ------------------------------------------------------ */
 enum { SGM_FLOW_NUM_STAGES = 3 };   /* propagation, random search, kNN */
 

@@ -11,5 +11,5 @@ from .oracle import (  # noqa: F401
     build, census, cost, path, aggregate, wta, lr_check, sgm_view, disparity,
     combine, reproject, evaluate, run_quad, run_stream, lib_path,
     FQ, FF_DEFAULTS, ff_downsample, ff_wht, ff_patch_cost, ff_knn_init, ff_rng, ff_sweep, ff_lift,
-    ff_field, ff_consistency, ff_flow, edge_distance, densify,
+    ff_field, ff_consistency, ff_flow, edge_distance, densify, densify_points,
 )

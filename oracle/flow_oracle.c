@@ -387,6 +387,39 @@ double orc_edge_distance(const uint8_t *G, int W, int H, int px, int py, int sx,
     return sqrt((double)dx * dx + (double)dy * dy) + lambda * (double)acc;
 }
 
+/* Densified value of one pixel (the body of orc_densify for a gap pixel). */
+static void densify_pixel(const float *field, const uint8_t *valid, const uint8_t *guide, int W, int H, int C,
+                          int K, double lambda, int px, int py, double *o)
+{
+    const int64_t n = (int64_t)W * H;
+    long long bd[64];
+    int64_t bi[64];
+    int cnt = 0;
+    for (int64_t q = 0; q < n; ++q) {              /* exhaustive: the K nearest seeds */
+        if (!valid[q]) continue;
+        const long long dx = q % W - px, dy = q / W - py;
+        const long long d = dx * dx + dy * dy;
+        if (cnt < K || d < bd[cnt - 1]) {
+            int pos = cnt < K ? cnt++ : K - 1;
+            while (pos > 0 && bd[pos - 1] > d) {
+                bd[pos] = bd[pos - 1];
+                bi[pos] = bi[pos - 1];
+                --pos;
+            }
+            bd[pos] = d;
+            bi[pos] = q;
+        }
+    }
+    double wsum = 0.0, acc[4] = {0, 0, 0, 0};
+    for (int k = 0; k < cnt; ++k) {
+        const int sx = (int)(bi[k] % W), sy = (int)(bi[k] / W);
+        const double w = 1.0 / orc_edge_distance(guide, W, H, px, py, sx, sy, lambda);
+        wsum += w;
+        for (int c = 0; c < C; ++c) acc[c] += w * field[bi[k] * C + c];
+    }
+    for (int c = 0; c < C; ++c) o[c] = cnt ? acc[c] / wsum : 0.0;
+}
+
 int orc_densify(const float *field, const uint8_t *valid, const uint8_t *guide, int W, int H, int C,
                 int K, double lambda, double *out)
 {
@@ -399,35 +432,24 @@ int orc_densify(const float *field, const uint8_t *valid, const uint8_t *guide, 
             for (int c = 0; c < C; ++c) out[p * C + c] = field[p * C + c];
             continue;
         }
-        for (int c = 0; c < C; ++c) out[p * C + c] = 0.0;
-        if (nseed == 0) continue;
-        const int px = (int)(p % W), py = (int)(p / W);
-        long long bd[64];
-        int64_t bi[64];
-        int cnt = 0;
-        for (int64_t q = 0; q < n; ++q) {          /* exhaustive: the K nearest seeds */
-            if (!valid[q]) continue;
-            const long long dx = q % W - px, dy = q / W - py;
-            const long long d = dx * dx + dy * dy;
-            if (cnt < K || d < bd[cnt - 1]) {
-                int pos = cnt < K ? cnt++ : K - 1;
-                while (pos > 0 && bd[pos - 1] > d) {
-                    bd[pos] = bd[pos - 1];
-                    bi[pos] = bi[pos - 1];
-                    --pos;
-                }
-                bd[pos] = d;
-                bi[pos] = q;
-            }
-        }
-        double wsum = 0.0, acc[4] = {0, 0, 0, 0};
-        for (int k = 0; k < cnt; ++k) {
-            const int sx = (int)(bi[k] % W), sy = (int)(bi[k] / W);
-            const double w = 1.0 / orc_edge_distance(guide, W, H, px, py, sx, sy, lambda);
-            wsum += w;
-            for (int c = 0; c < C; ++c) acc[c] += w * field[bi[k] * C + c];
-        }
-        for (int c = 0; c < C; ++c) out[p * C + c] = acc[c] / wsum;
+        densify_pixel(field, valid, guide, W, H, C, K, lambda, (int)(p % W), (int)(p / W), out + p * C);
     }
     return nseed == 0 ? 3 : 0;
+}
+
+/* The same at a list of pixels xy[npts][2] (for parity samples of full-size images). */
+int orc_densify_points(const float *field, const uint8_t *valid, const uint8_t *guide, int W, int H, int C,
+                       int K, double lambda, int npts, const int *xy, double *out)
+{
+    if (K < 1 || K > 64 || C < 1 || C > 4) return 1;
+    for (int i = 0; i < npts; ++i) {
+        const int x = xy[2 * i], y = xy[2 * i + 1];
+        const int64_t p = (int64_t)y * W + x;
+        if (valid[p]) {
+            for (int c = 0; c < C; ++c) out[i * C + c] = field[p * C + c];
+        } else {
+            densify_pixel(field, valid, guide, W, H, C, K, lambda, x, y, out + i * C);
+        }
+    }
+    return 0;
 }

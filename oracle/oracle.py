@@ -74,6 +74,8 @@ def _get():
             lib.orc_edge_distance.restype = Dd
             lib.orc_densify.argtypes = [P, P, P, I, I, I, I, Dd, P]
             lib.orc_densify.restype = ctypes.c_int
+            lib.orc_densify_points.argtypes = [P, P, P, I, I, I, I, Dd, I, P, P]
+            lib.orc_densify_points.restype = ctypes.c_int
             for fn in ("orc_ff_downsample", "orc_ff_wht", "orc_ff_knn_init", "orc_ff_sweep",
                        "orc_ff_lift", "orc_ff_field", "orc_ff_consistency", "orc_ff_flow"):
                 getattr(lib, fn).restype = ctypes.c_int
@@ -423,4 +425,19 @@ def densify(field, valid, guide, K=25, lam=1.0):
     if rc == 3:
         raise ValueError("densify: no valid pixel")
     _chk(rc, "densify")
+    return out
+
+
+def densify_points(field, valid, guide, xy, K=25, lam=1.0):
+    """densify at the pixels xy [m][2] (x, y) only: float64 [m][C]."""
+    field = _c(field, np.float32)
+    if field.ndim == 2:
+        field = field[..., None]
+    valid = _c(valid, np.uint8)
+    guide = _c(guide, np.uint8)
+    xy = _c(xy, np.int32)
+    H, W, C = field.shape
+    out = np.empty((len(xy), C), np.float64)
+    _chk(_get().orc_densify_points(_p(field), _p(valid), _p(guide), W, H, C, K, lam, len(xy), _p(xy),
+                                   _p(out)), "densify_points")
     return out

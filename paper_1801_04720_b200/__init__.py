@@ -6,13 +6,13 @@ does not touch the GPU; creating an ``SGM`` loads the library and fails loudly
 if it is missing (there is no CPU fallback).
 """
 __all__ = ["SGM", "Camera", "stack_quads", "pitch_for", "rates_from_counts", "stack_video",
-           "FlowFields"]
+           "FlowFields", "densify"]
 
 
 def __getattr__(name):
-    if name == "FlowFields":
+    if name in ("FlowFields", "densify"):
         from . import flow
-        return flow.FlowFields
+        return getattr(flow, name)
     if name in __all__:
         from . import sgm
         return getattr(sgm, name)

@@ -94,6 +94,16 @@ struct FFFields {
     int32_t *cost;                 // [nfields][H][W]
 };
 
+// Densification (densify.cu): n images of W x H, C channels
+struct DensifyParams {
+    int n, W, H, C, K;
+    float lambda;
+    const float *field;            // [n][H][W][C]
+    const uint8_t *valid, *guide;  // [n][H][W]
+    float *out;                    // [n][H][W][C]
+    int *unfilled;                 // nullable: pixels left without a seed
+};
+
 // ----------------------------------------------------------------- launchers (host)
 cudaError_t launch_census(const uint8_t *const *imgs, int nimg, long long pitch, int W, int H,
                           int cw, int ch, uint64_t *out, long long out_stride, cudaStream_t st);
@@ -109,6 +119,7 @@ cudaError_t launch_repitch(const uint8_t *src, uint8_t *dst, int W, long long pi
                            cudaStream_t st);
 cudaError_t launch_combine(const CombineParams &p, cudaStream_t st);
 cudaError_t launch_evaluate(const EvalParams &p, cudaStream_t st);
+cudaError_t launch_densify(const DensifyParams &p, cudaStream_t st);
 int evaluate_max_blocks();   // scratch rows launch_evaluate may use besides one per quad
 cudaError_t ff_launch_downsample(const uint8_t *src, long long src_stride, int W, int H, uint8_t *dst,
                                  long long dst_stride, int nimg, cudaStream_t st);

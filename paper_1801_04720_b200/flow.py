@@ -120,3 +120,20 @@ class FlowFields:
         _lib.call("sgm_flow_consistency", self.h, _ptr(F), _ptr(G1), _ptr(G2), w, h, _ptr(v),
                   _stream(stream))
         return v
+
+
+def densify(field, valid, guide, K=25, lam=1.0, stream=None, count_unfilled=False):
+    """Edge-aware densification (sgm_densify): field float32 [n][H][W][C] (or [H][W][C]),
+    valid / guide uint8 [n][H][W] (device).  Returns the dense field (and the number of
+    pixels of images without seeds if asked)."""
+    squeeze = field.dim() == 3
+    if squeeze:
+        field, valid, guide = field[None], valid[None], guide[None]
+    field = field.contiguous()
+    n, H, W, C = field.shape
+    out = torch.empty_like(field)
+    cnt = torch.zeros((1,), dtype=torch.int32, device=field.device) if count_unfilled else None
+    _lib.call("sgm_densify", n, W, H, C, _ptr(field), _ptr(valid.contiguous()), _ptr(guide.contiguous()),
+              int(K), float(lam), _ptr(out), _ptr(cnt), _stream(stream))
+    out = out[0] if squeeze else out
+    return (out, cnt) if count_unfilled else out

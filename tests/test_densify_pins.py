@@ -121,3 +121,15 @@ def test_brute_force(orc, seed):
 def test_no_seed_is_an_error(orc):
     with pytest.raises(ValueError):
         orc.densify(np.zeros((4, 4, 2), np.float32), np.zeros((4, 4), np.uint8), np.zeros((4, 4), np.uint8))
+
+
+def test_points_equal_full(orc):
+    rng = np.random.default_rng(4)
+    H, W = 13, 17
+    f = rng.normal(0, 3, (H, W, 2)).astype(np.float32)
+    v = (rng.random((H, W)) < 0.4).astype(np.uint8)
+    g = synth.translated_pair(W, H, 5, 0, 0)[0]
+    full = orc.densify(f, v, g, K=9)
+    xy = np.stack([rng.integers(0, W, 30), rng.integers(0, H, 30)], 1)
+    pts = orc.densify_points(f, v, g, xy, K=9)
+    assert np.array_equal(pts, full[xy[:, 1], xy[:, 0]])
