@@ -6,9 +6,11 @@
 // interior points of the segment p -> s).
 //
 // One thread per pixel.  The K nearest seeds come from a ring search: rings of Chebyshev
-// radius r = 1, 2, ... are enumerated and offered to a (distance^2 << 32 | index)-keyed
-// top-K list; the search stops once K seeds are held and r^2 exceeds the K-th distance^2
-// (every later pixel is at least r away), which is exactly the exhaustive result.
+// radius r = 1, 2, ... are enumerated (sides without any valid pixel skipped in O(1) with
+// per-row / per-column prefix counts, so wide holes cost O(radius)) and offered to a
+// (distance^2 << 32 | index)-keyed top-K list; the search stops once K seeds are held and
+// r^2 exceeds the K-th distance^2 (every later pixel is at least r away), which is exactly
+// the exhaustive result.
 #include "sgm_internal.cuh"
 
 namespace sgm {
@@ -20,12 +22,6 @@ __device__ __forceinline__ int grad_l1(const uint8_t *__restrict__ G, int W, int
     const int gx = int(__ldg(G + (long long)y * W + min(x + 1, W - 1))) - int(__ldg(G + (long long)y * W + max(x - 1, 0)));
     const int gy = int(__ldg(G + (long long)min(y + 1, H - 1) * W + x)) - int(__ldg(G + (long long)max(y - 1, 0) * W + x));
     return abs(gx) + abs(gy);
-}
-
-// round-half-up of a / b, b > 0
-__device__ __forceinline__ int div_round(int a, int b) {
-    const int num = 2 * a + b, den = 2 * b;
-    return num >= 0 ? num / den : -((-num + den - 1) / den);
 }
 
 struct SeedList {
@@ -42,7 +38,58 @@ __device__ __noinline__ unsigned long long seed_insert(SeedList *L, int &cnt, in
     return cnt == K ? L->key[K - 1] : ~0ull;
 }
 
-__global__ void densify_kernel(const DensifyParams p) {
+// Per-image prefix counts of valid pixels along rows (rowc[img][y][x] = #valid in row y,
+// columns < x; W+1 entries per row) and along columns (colc[img][x][y], H+1 per column):
+// the ring search skips empty ring sides in O(1).
+__global__ void densify_rowcount_kernel(const DensifyParams p, int *__restrict__ rowc) {
+    const int rows = p.H * p.n;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        const uint8_t *v = p.valid + (long long)r * p.W;
+        int *o = rowc + (long long)r * (p.W + 1);
+        int c = 0;
+        o[0] = 0;
+        for (int x = 0; x < p.W; ++x) { c += v[x] != 0; o[x + 1] = c; }
+    }
+}
+// the guide's L1 gradient g(q) per pixel (DN3), so a segment walk reads one value per step
+__global__ void densify_grad_kernel(const DensifyParams p, uint16_t *__restrict__ grad) {
+    const long long per = (long long)p.W * p.H, total = per * p.n;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int img = int(t / per);
+        const long long q = t - img * per;
+        const int y = int(q / p.W), x = int(q - (long long)y * p.W);
+        grad[t] = uint16_t(grad_l1(p.guide + img * per, p.W, p.H, x, y));
+    }
+}
+
+__global__ void densify_colcount_kernel(const DensifyParams p, int *__restrict__ colc) {
+    const int cols = p.W * p.n;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cols; t += gridDim.x * blockDim.x) {
+        const int img = t / p.W, x = t - img * p.W;
+        const uint8_t *v = p.valid + (long long)img * p.W * p.H + x;
+        int *o = colc + ((long long)img * p.W + x) * (p.H + 1);
+        int c = 0;
+        o[0] = 0;
+        for (int y = 0; y < p.H; ++y) { c += v[(long long)y * p.W] != 0; o[y + 1] = c; }
+    }
+}
+
+// floor((2 k a + n) / (2 n)) for k = 1, 2, ... (round-half-up of k a / n), stepped
+// incrementally: quotient q and remainder m of (2 k a + n) by 2 n, |2 a| <= 2 n
+struct RoundStep {
+    int q, m, a2, n2;
+    __device__ __forceinline__ RoundStep(int a, int n) : q(0), m(n), a2(2 * a), n2(2 * n) {}
+    __device__ __forceinline__ int next() {
+        m += a2;
+        if (m >= n2) { m -= n2; ++q; }
+        else if (m < 0) { m += n2; --q; }
+        return q;
+    }
+};
+
+__global__ void densify_kernel(const DensifyParams p, const int *__restrict__ rowc, const int *__restrict__ colc,
+                               const uint16_t *__restrict__ grad) {
     const long long per = (long long)p.W * p.H, total = per * p.n;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
@@ -62,16 +109,25 @@ __global__ void densify_kernel(const DensifyParams p) {
         const int rmax = max(p.W, p.H);
         for (int r = 1; r <= rmax; ++r) {
             if (cnt == p.K && (unsigned long long)r * r > (kth >> 32)) break;
-            // ring of Chebyshev radius r: rows y - r, y + r (full), columns x - r, x + r
+            // ring of Chebyshev radius r: rows y - r, y + r (full), columns x - r, x + r;
+            // each side is clipped to the image and skipped when its prefix count is zero
             for (int side = 0; side < 4; ++side) {
-                const int len = side < 2 ? 2 * r + 1 : 2 * r - 1;
-                for (int k = 0; k < len; ++k) {
-                    int sx, sy;
-                    if (side == 0) { sx = x - r + k; sy = y - r; }
-                    else if (side == 1) { sx = x - r + k; sy = y + r; }
-                    else if (side == 2) { sx = x - r; sy = y - r + 1 + k; }
-                    else { sx = x + r; sy = y - r + 1 + k; }
-                    if (sx < 0 || sy < 0 || sx >= p.W || sy >= p.H) continue;
+                int fixed, lo, hi;                  // the side's fixed coordinate and range
+                if (side < 2) {
+                    fixed = side == 0 ? y - r : y + r;
+                    if (fixed < 0 || fixed >= p.H) continue;
+                    lo = max(x - r, 0); hi = min(x + r, p.W - 1);
+                    const int *rc = rowc + ((long long)img * p.H + fixed) * (p.W + 1);
+                    if (lo > hi || rc[hi + 1] == rc[lo]) continue;
+                } else {
+                    fixed = side == 2 ? x - r : x + r;
+                    if (fixed < 0 || fixed >= p.W) continue;
+                    lo = max(y - r + 1, 0); hi = min(y + r - 1, p.H - 1);
+                    const int *cc = colc + ((long long)img * p.W + fixed) * (p.H + 1);
+                    if (lo > hi || cc[hi + 1] == cc[lo]) continue;
+                }
+                for (int k = lo; k <= hi; ++k) {
+                    const int sx = side < 2 ? k : fixed, sy = side < 2 ? fixed : k;
                     const long long sq = (long long)sy * p.W + sx;
                     if (!valid[sq]) continue;
                     const int dx = sx - x, dy = sy - y;
@@ -88,8 +144,12 @@ __global__ void densify_kernel(const DensifyParams p) {
             const int dx = sx - x, dy = sy - y;
             const int n = max(abs(dx), abs(dy));
             int g = 0;
-            for (int j = 1; j < n; ++j)
-                g += grad_l1(p.guide + img * per, p.W, p.H, x + div_round(j * dx, n), y + div_round(j * dy, n));
+            RoundStep rx(dx, n), ry(dy, n);
+            const uint16_t *gi = grad + img * per;
+            for (int j = 1; j < n; ++j) {
+                const int qx = x + rx.next(), qy = y + ry.next();
+                g += __ldg(gi + (long long)qy * p.W + qx);
+            }
             const float w = 1.0f / (sqrtf(float(dx * dx + dy * dy)) + p.lambda * float(g));
             wsum += w;
             for (int c = 0; c < p.C; ++c) acc[c] = fmaf(w, field[(long long)sq * p.C + c], acc[c]);
@@ -107,15 +167,30 @@ __global__ void densify_kernel(const DensifyParams p) {
 
 cudaError_t launch_densify(const DensifyParams &p, cudaStream_t st) {
     if (p.K < 1 || p.K > kDensifyKMax) return cudaErrorInvalidValue;
-    if (p.unfilled) {
-        cudaError_t e = cudaMemsetAsync(p.unfilled, 0, sizeof(int), st);
-        if (e != cudaSuccess) return e;
-    }
+    cudaError_t e = cudaSuccess;
+    if (p.unfilled) e = cudaMemsetAsync(p.unfilled, 0, sizeof(int), st);
+    // prefix counts in stream-ordered scratch
+    const size_t rown = size_t(p.n) * p.H * (p.W + 1), coln = size_t(p.n) * p.W * (p.H + 1);
+    const size_t npx = size_t(p.n) * p.W * p.H;
+    int *scratch = nullptr;
+    if (e == cudaSuccess)
+        e = cudaMallocAsync(reinterpret_cast<void **>(&scratch), sizeof(int) * (rown + coln) + 2 * npx + 16, st);
+    if (e != cudaSuccess) return e;
+    int *rowc = scratch, *colc = scratch + rown;
+    uint16_t *grad = reinterpret_cast<uint16_t *>(colc + coln);
+    densify_rowcount_kernel<<<(p.H * p.n + 127) / 128, 128, 0, st>>>(p, rowc);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) densify_colcount_kernel<<<(p.W * p.n + 127) / 128, 128, 0, st>>>(p, colc);
+    if (e == cudaSuccess) e = cudaGetLastError();
     const long long total = (long long)p.W * p.H * p.n;
     long long g = (total + 127) / 128;
     if (g > 148LL * 32) g = 148LL * 32;
-    densify_kernel<<<unsigned(g < 1 ? 1 : g), 128, 0, st>>>(p);
-    return cudaGetLastError();
+    if (e == cudaSuccess) densify_grad_kernel<<<unsigned(g < 1 ? 1 : g), 128, 0, st>>>(p, grad);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) densify_kernel<<<unsigned(g < 1 ? 1 : g), 128, 0, st>>>(p, rowc, colc, grad);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    const cudaError_t e2 = cudaFreeAsync(scratch, st);
+    return e != cudaSuccess ? e : e2;
 }
 
 }  // namespace sgm
