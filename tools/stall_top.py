@@ -27,7 +27,8 @@ for k, v in data.items():
             agg[c] += int(d[c] or 0)
     S = sum(agg.values()) or 1
     tot = sum(int(d["Instructions Executed"] or 0) for d in u)
-    print("==", k[:100], "instructions", tot)
+    allsamp = sum(int(d["Warp Stall Sampling (All Samples)"] or 0) for d in u)
+    print("==", k[:100], "instructions", tot, "samples", allsamp)
     print("   " + ", ".join(f"{c[6:]}={v / S * 100:.1f}%" for c, v in agg.most_common(10)))
     for d in sorted(u, key=lambda d: -int(d["Warp Stall Sampling (All Samples)"] or 0))[:N]:
         reason = max(cols, key=lambda c: int(d[c] or 0))
