@@ -535,6 +535,7 @@ __global__ void ff_init_kernel(FieldSet fs, const int32_t *__restrict__ nn, int 
         int best = 0x7fffffff, bu = 0, bv = 0;
         for (int k = 0; k < knn; ++k) {
             const int q = cand[k];
+            if (q < 0 || q >= per) continue;        // fewer database pixels than knn
             const int yb = q / fs.W, xb = q - yb * fs.W;
             const int fu = (xb - x) * FQ, fv = (yb - y) * FQ;
             const int c = patch_cost_thread(src, dst, fs.W, fs.H, x, y, fu, fv, fs.rad(kind), fs.pen64);

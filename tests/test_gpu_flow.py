@@ -158,3 +158,18 @@ def test_flow_deterministic_and_feeds_scene_flow(dev):
     assert not (vs & ~v).any()
     g.close()
     ff.close()
+
+
+@pytest.mark.parametrize("shape,levels", [((1, 40), 3), ((40, 1), 3), ((3, 2), 2), ((2, 2), 1),
+                                          ((17, 5), 4)], ids=str)
+def test_flow_degenerate_shapes(orc, dev, shape, levels):
+    """Single-row / single-column images, a 1x1 coarsest level, fewer pixels than kNN
+    candidates' tiles: the whole flow stays bit-exact."""
+    W, H = shape
+    A, B = synth.translated_pair(W, H, 50 + W + H, 1, 0)
+    ff = _ff(W, H, levels=levels, knn=4)
+    out = ff.flow(_t(A[None], dev), _t(B[None], dev), want_fields=True)
+    of, ov = orc.ff_flow(A, B, levels=levels)
+    assert np.array_equal(out["fields_q"][0, 0].cpu().numpy(), of)
+    assert np.array_equal(out["valid"][0].cpu().numpy(), ov)
+    ff.close()
