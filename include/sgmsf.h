@@ -92,7 +92,7 @@ typedef struct sgm_sceneflow_out {
 
 /* Create a handle on `device` (cudaSetDevice is called): validates `p`
  * (SGM_ERR_INVALID_ARGUMENT on: W or H < 1, D outside 1..256, even census
- * side, census_w*census_h-1 > 63, P1 < 0, P2 < P1, C_max+P2 > 255, T < 0,
+ * side, a 1x1 census window (no bits), census_w*census_h-1 > 63, P1 < 0, P2 < P1, C_max+P2 > 255, T < 0,
  * bilinear_rule not 0/1, max_batch < 1) and allocates all scratch for
  * max_batch quads (SGM_ERR_OUT_OF_MEMORY if that fails).  Synchronous.
  * `*out` is set only on SGM_OK. */

@@ -53,6 +53,7 @@ GOOD = dict(width=64, height=48, num_disp=16, census_w=5, census_h=5, p1=10, p2=
     ("width", 0), ("height", -1), ("num_disp", 0), ("num_disp", 257),
     ("census_w", 4), ("census_h", 6), ("census_w", 11),          # 11*7-1 > 63 bits
     ("census_w", 13),                                            # 13*5-1 = 64 > 63 bits
+    ("census_w", 1),                                             # with census_h = 1: no bits
     ("p1", -1), ("p2", 5),                                       # P2 < P1 (G8)
     ("p2", 240),                                                 # C_max + P2 > 255 (G9)
     ("lr_threshold", -1), ("bilinear_rule", 2), ("max_batch", 0),
@@ -64,6 +65,8 @@ def test_create_rejects_invalid_params(field, value):
         kw["census_h"] = 7
     if field == "census_w" and value == 13:
         kw["census_h"] = 5
+    if field == "census_w" and value == 1:
+        kw["census_h"] = 1
     kw[field] = value
     p = _lib.SgmParams(**kw)
     h = ctypes.c_void_p()

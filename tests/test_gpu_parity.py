@@ -46,6 +46,16 @@ SHAPES = [
     (40, 20, 64, 5, 5, 3, 9),         # W < D (border everywhere)
     (33, 1, 32, 3, 3, 2, 20),         # single row
     (1, 9, 16, 3, 3, 2, 20),          # single column
+    # edge cases of the parameters: one / two disparity levels, D just past a CPL step,
+    # D = 255, a 3x1 census (2 bits), tall and wide census windows, P1 = P2 = 0
+    (45, 17, 1, 5, 5, 4, 30),
+    (45, 17, 2, 5, 5, 4, 30),
+    (90, 19, 65, 9, 7, 7, 86),
+    (280, 13, 255, 9, 7, 7, 86),
+    (37, 15, 16, 3, 1, 1, 5),
+    (61, 23, 32, 7, 9, 7, 86),
+    (61, 23, 32, 13, 3, 5, 60),
+    (48, 21, 24, 3, 3, 0, 0),
 ]
 
 
