@@ -665,20 +665,26 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
 #pragma unroll
     for (int k = 0; k < NK; ++k) aoff[k] = (long long)clampi(y + sdy[k], 0, H - 1) * W;
     int2 hv = make_int2(0, 0);                      // vector of the previous pixel in scan order
-    unsigned long long hbuf = 0ull;                 // band handoff entries hbase + lane
-    int hbase = 0;
-    // incumbent of the next position, loaded one position ahead
-    int nx0 = fwd ? 0 : W - 1;
-    long long np = (long long)y * W + nx0;
-    int ncu = flow[2 * np], ncv = flow[2 * np + 1], ncc = cost[np];
+    unsigned long long hbuf = 0ull;                 // band handoff entries of the chunk (lane l)
+    // The incumbents (vector + cost) of 32 positions are loaded per chunk, lane l holding
+    // position 32c + l, one chunk ahead: no global load latency on the row's chain.
+    auto chunk_px = [&](int i) { return (long long)y * W + (fwd ? i : W - 1 - i); };
+    int cu_l = 0, cv_l = 0, cc_l = 0, nu_l = 0, nv_l = 0, nc_l = 0;
+    if (lane < W) { const long long q = chunk_px(lane); cu_l = flow[2 * q]; cv_l = flow[2 * q + 1]; cc_l = cost[q]; }
+    if (32 + lane < W) { const long long q = chunk_px(32 + lane); nu_l = flow[2 * q]; nv_l = flow[2 * q + 1]; nc_l = cost[q]; }
     for (int i = 0; i < W; ++i) {
         const int x = fwd ? i : W - 1 - i;
         const long long p = (long long)y * W + x;
-        int cu = ncu, cv = ncv, cc = ncc;
-        if (i + 1 < W) {
-            np = p + (fwd ? 1 : -1);
-            ncu = flow[2 * np]; ncv = flow[2 * np + 1]; ncc = cost[np];
+        if ((i & 31) == 0 && i > 0) {               // next chunk: rotate and prefetch
+            cu_l = nu_l; cv_l = nv_l; cc_l = nc_l;
+            if (i + 32 + lane < W) {
+                const long long q = chunk_px(i + 32 + lane);
+                nu_l = flow[2 * q]; nv_l = flow[2 * q + 1]; nc_l = cost[q];
+            }
         }
+        int cu = __shfl_sync(0xffffffffu, cu_l, i & 31);
+        int cv = __shfl_sync(0xffffffffu, cv_l, i & 31);
+        int cc = __shfl_sync(0xffffffffu, cc_l, i & 31);
         // vertical candidate: the finished vector of (x, row above in scan order)
         int2 vv = make_int2(0, 0);
         if (has_above) {
@@ -688,18 +694,17 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
                 // warps that have work
                 while (hand_tag(e = ring_in[i & (kRowRing - 1)]) != i + 1) __nanosleep(20);
             } else {
-                // band handoff through L2: fetch 32 positions per round trip (lane l holds
-                // position hbase + l) and re-poll only when the producer is not there yet
+                // band handoff through L2: wait until the whole 32-position chunk is
+                // published, one round trip per poll, then read it from registers
                 if ((i & 31) == 0) {
-                    hbase = i;
-                    hbuf = hbase + lane < W ? ld_relaxed_u64(hin + hbase + lane) : 0ull;
+                    while (true) {
+                        hbuf = i + lane < W ? ld_relaxed_u64(hin + i + lane) : 0ull;
+                        const bool ready = i + lane >= W || hand_tag(hbuf) == i + lane + 1;
+                        if (__all_sync(0xffffffffu, ready)) break;
+                        __nanosleep(128);
+                    }
                 }
                 e = __shfl_sync(0xffffffffu, hbuf, i & 31);
-                while (hand_tag(e) != i + 1) {
-                    __nanosleep(64);
-                    hbuf = hbase + lane < W ? ld_relaxed_u64(hin + hbase + lane) : 0ull;
-                    e = __shfl_sync(0xffffffffu, hbuf, i & 31);
-                }
             }
             vv = hand_vec(e);
         }
@@ -769,7 +774,9 @@ __global__ void __launch_bounds__(NW * 32) ff_prop_kernel(const PropParams pp) {
     if (threadIdx.x == 0) s_ticket = atomicAdd(pp.ticket, 1);
     __syncthreads();
     const int ticket = s_ticket;
-    const int f = ticket / pp.nbands, band = ticket - f * pp.nbands;
+    // band-major tickets: the resident CTAs are the first bands of all fields, so a band's
+    // predecessor (one ticket "row" earlier) has normally finished before it starts
+    const int band = ticket / pp.fs.nfields, f = ticket - band * pp.fs.nfields;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = band * NW + warp;                 // iteration row
     if (j >= pp.fs.H) return;
