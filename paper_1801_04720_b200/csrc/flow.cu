@@ -568,7 +568,7 @@ __global__ void ff_lift_kernel(FieldSet fs, const int32_t *__restrict__ coarse, 
 }
 
 // random search (FF7, second half): reads only the pixel's own vector
-__global__ void ff_search_kernel(FieldSet fs, int sweep, int level, int R0) {
+__global__ void __launch_bounds__(128, 6) ff_search_kernel(FieldSet fs, int sweep, int level, int R0) {
     const long long per = (long long)fs.W * fs.H, total = per * fs.nfields;
     const int R = max(R0 >> sweep, 1);
     const unsigned span = unsigned(2 * R * FQ + 1);
