@@ -173,3 +173,16 @@ def test_flow_degenerate_shapes(orc, dev, shape, levels):
     assert np.array_equal(out["fields_q"][0, 0].cpu().numpy(), of)
     assert np.array_equal(out["valid"][0].cpu().numpy(), ov)
     ff.close()
+
+
+@pytest.mark.slow
+def test_flow_highres_full_size(orc, dev):
+    """BASELINE configs[3] size (2048x1024), 4 levels: every vector and mask bit."""
+    q = synth.make_quad("highres", 0)
+    H, W = q["il0"].shape
+    ff = _ff(W, H, levels=4)
+    out = ff.flow(_t(q["il0"][None], dev), _t(q["il1"][None], dev), want_fields=True)
+    of, ov = orc.ff_flow(q["il0"], q["il1"], levels=4)
+    assert np.array_equal(out["fields_q"][0, 0].cpu().numpy(), of)
+    assert np.array_equal(out["valid"][0].cpu().numpy(), ov)
+    ff.close()

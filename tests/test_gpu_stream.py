@@ -44,7 +44,8 @@ def _stream_vs_quads(g, video, cam, dev):
     return out
 
 
-@pytest.mark.parametrize("name,n", [("tiny", 5), ("driving", 3)])
+@pytest.mark.parametrize("name,n", [("tiny", 5), ("driving", 3),
+                                    pytest.param("wide", 2, marks=pytest.mark.slow)])
 def test_stream_parity(orc, dev, name, n):
     from paper_1801_04720_b200 import SGM, Camera
     cfg = synth.CONFIGS[name]
