@@ -696,7 +696,7 @@ cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cud
 
 }  // namespace
 
-int sweep_warps_for(int cpl) { return cpl <= 4 ? 16 : 8; }
+int sweep_warps_for(int cpl) { return cpl <= 6 ? 16 : 8; }
 
 cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool debug_s,
                           cudaStream_t st, cudaEvent_t mid_ev_a, cudaEvent_t mid_ev_b,
@@ -708,9 +708,9 @@ cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool 
 #define SGM_CASE(CPL_, C64_)                                                                   \
     if (cpl == CPL_ && c64 == C64_) {                                                          \
         if (p.D < 32 * CPL_)                                                                   \
-            return launch_pair<CPL_, C64_, (CPL_ <= 4 ? 16 : 8), true>(                        \
+            return launch_pair<CPL_, C64_, (CPL_ <= 6 ? 16 : 8), true>(                        \
                 p, debug_s, st, mid_ev_a, mid_ev_b, launches, sync_buf, sync_bytes);           \
-        return launch_pair<CPL_, C64_, (CPL_ <= 4 ? 16 : 8), false>(                           \
+        return launch_pair<CPL_, C64_, (CPL_ <= 6 ? 16 : 8), false>(                           \
             p, debug_s, st, mid_ev_a, mid_ev_b, launches, sync_buf, sync_bytes);               \
     }
     SGM_CASE(2, false) SGM_CASE(2, true) SGM_CASE(4, false) SGM_CASE(4, true)
