@@ -165,12 +165,16 @@ struct Sweep {
     static constexpr int RS = (CPL <= 4) ? kRingWide : kRing;
     static constexpr int G = (CPL <= 4) ? CPL : 1;   // groups align with the unrolled block
     static constexpr int RG = RS / G;              // groups per ring
+    // band-input ring of warp 0 (positions) and census prefetch entries per warp: trimmed
+    // for 8 cells per lane so that 16-row bands fit the 227 KB of shared memory
+    static constexpr int RING0 = (CPL <= 6) ? kRing0 : kRing0 / 2;
+    static constexpr int CEN = BWD ? 0 : 64;       // the backward sweep reads no census
 
     static constexpr size_t smem_bytes() {
         size_t b = 0;
         b += size_t(NW) * RS * VEC * 2;             // ring
-        b += size_t(kRing0) * VEC * 2;              // band input ring
-        b += size_t(NW) * 2 * 64 * 8;               // census prefetch (ref, fresh)
+        b += size_t(RING0) * VEC * 2;               // band input ring
+        b += size_t(NW) * 2 * CEN * 8;              // census prefetch (ref, fresh)
         if (BWD) {
             b += size_t(NW) * DP * 2;               // WTA scratch
         }
@@ -215,8 +219,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint16_t *ring = reinterpret_cast<uint16_t *>(smem_raw);
     uint16_t *in0 = ring + size_t(NW) * RS * VEC;
-    uint64_t *cbuf = reinterpret_cast<uint64_t *>(in0 + size_t(kRing0) * VEC);
-    uint16_t *wsc = reinterpret_cast<uint16_t *>(cbuf + size_t(NW) * 2 * 64);
+    constexpr int RING0 = SW::RING0;
+    uint64_t *cbuf = reinterpret_cast<uint64_t *>(in0 + size_t(RING0) * VEC);
+    uint16_t *wsc = reinterpret_cast<uint16_t *>(cbuf + size_t(NW) * 2 * SW::CEN);
     uint64_t *bars = reinterpret_cast<uint64_t *>(wsc + (BWD ? size_t(NW) * DP : 0));
     // full[w][s]: slot s of warp w's ring holds complete data (32 producer lanes arrive)
     // empty[w][s]: the consumer (warp w+1) is done with slot s (32 consumer lanes arrive)
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     // L = C, i.e. every slot nobody writes acts as a path start.
     {
         uint4 *z = reinterpret_cast<uint4 *>(smem_raw);
-        const int n16 = int((size_t(NW) * RS + kRing0) * VEC * 2 / 16);
+        const int n16 = int((size_t(NW) * RS + RING0) * VEC * 2 / 16);
         const uint32_t ps = uint32_t(p.P1) * 0x10001u;     // biased path-start vector
         for (int k = threadIdx.x; k < n16; k += (NW + 1) * 32) z[k] = make_uint4(ps, ps, ps, ps);
     }
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     constexpr int kChunks = VEC * 2 / 16;           // 16-byte chunks per position
 
     // cp.async the band input of positions [hG, hG+G) (gbuf -> in0), one commit group
-    constexpr int LG = (kRing0 / G - 1) > 2 ? 2 : (kRing0 / G - 1);   // prefetch distance (groups)
+    constexpr int LG = (RING0 / G - 1) > 2 ? 2 : (RING0 / G - 1);     // prefetch distance (groups)
     auto issue_input = [&](int h) {
         const int q0 = h * G;
         if (q0 < W) {
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             const char *g = reinterpret_cast<const char *>(gin + (long long)q0 * VEC) + 16 * lane;
 #pragma unroll 1
             for (int q = q0; q < q0 + G && q < W; ++q, g += 2 * VEC) {
-                char *sm = reinterpret_cast<char *>(in0 + size_t(q & (kRing0 - 1)) * VEC) + 16 * lane;
+                char *sm = reinterpret_cast<char *>(in0 + size_t(q & (RING0 - 1)) * VEC) + 16 * lane;
 #pragma unroll
                 for (int c = 0; c < kChunks; c += 32)
                     if (c + lane < kChunks) cp_async16(sm + 16 * c, g + 16 * c);
@@ -526,7 +531,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             // --- row-above predecessors: all three live in slot i
             uint32_t pv[3][R];
             {
-                const uint16_t *src = src_ring + size_t(i & (band_input || warp == 0 ? kRing0 - 1 : RS - 1)) * VEC;
+                const uint16_t *src = src_ring + size_t(i & (band_input || warp == 0 ? RING0 - 1 : RS - 1)) * VEC;
 #pragma unroll
                 for (int v = 0; v < 3; ++v) VecIO<R>::ld(src + v * DP, pv[v]);
             }
@@ -696,7 +701,7 @@ cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cud
 
 }  // namespace
 
-int sweep_warps_for(int cpl) { return cpl <= 6 ? 16 : 8; }
+int sweep_warps_for(int cpl) { (void)cpl; return 16; }
 
 cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool debug_s,
                           cudaStream_t st, cudaEvent_t mid_ev_a, cudaEvent_t mid_ev_b,
@@ -708,9 +713,9 @@ cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool 
 #define SGM_CASE(CPL_, C64_)                                                                   \
     if (cpl == CPL_ && c64 == C64_) {                                                          \
         if (p.D < 32 * CPL_)                                                                   \
-            return launch_pair<CPL_, C64_, (CPL_ <= 6 ? 16 : 8), true>(                        \
+            return launch_pair<CPL_, C64_, 16, true>(                        \
                 p, debug_s, st, mid_ev_a, mid_ev_b, launches, sync_buf, sync_bytes);           \
-        return launch_pair<CPL_, C64_, (CPL_ <= 6 ? 16 : 8), false>(                           \
+        return launch_pair<CPL_, C64_, 16, false>(                           \
             p, debug_s, st, mid_ev_a, mid_ev_b, launches, sync_buf, sync_bytes);               \
     }
     SGM_CASE(2, false) SGM_CASE(2, true) SGM_CASE(4, false) SGM_CASE(4, true)
