@@ -409,7 +409,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     for (int k = 0; k < CPL; ++k) win[k] = 0;
     // BWD: S_fwd register prefetch PF positions ahead (slot = position mod PF must be a
     // compile-time index, so PF divides the unroll CPL)
-    constexpr int PF = (CPL % 4 == 0) ? 4 : 2;
+    constexpr int PF = (CPL == 4) ? 4 : 2;
     uint32_t pf[PF][R];
 #pragma unroll
     for (int k = 0; k < PF; ++k)
