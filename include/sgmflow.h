@@ -80,10 +80,18 @@ SGM_API sgm_status sgm_flow(sgm_flow_handle *h, int32_t n, const uint8_t *frames
  *   field, out [n][H][W][C] float32 (C = 1..4: flow (u, v), scene flow (u, v, d0, d1), ...);
  *   valid, guide [n][H][W] uint8; 1 <= K <= 64; lambda >= 0 (gray levels -> px, 1.0);
  *   unfilled (device int32, nullable): number of pixels of images without any valid pixel
- *   (their output is 0, the SPEC's "zero valid pixels" error).  Arithmetic in float32. */
+ *   (their output is 0, the SPEC's "zero valid pixels" error);
+ *   scratch: device, 16-byte aligned, scratch_bytes >= sgm_densify_scratch_bytes(n, W, H)
+ *   (row / column prefix counts and the guide gradient); NULL = a stream-ordered allocation
+ *   inside the call (slower, and not capturable in every CUDA-graph setting).
+ * Arithmetic in float32. */
 SGM_API sgm_status sgm_densify(int32_t n, int32_t width, int32_t height, int32_t channels,
                        const float *field, const uint8_t *valid, const uint8_t *guide,
-                       int32_t K, float lambda, float *out, int32_t *unfilled, void *stream);
+                       int32_t K, float lambda, float *out, int32_t *unfilled, void *scratch,
+                       int64_t scratch_bytes, void *stream);
+
+/* Scratch bytes sgm_densify needs for n images of width x height (-1 if invalid). */
+SGM_API int64_t sgm_densify_scratch_bytes(int32_t n, int32_t width, int32_t height);
 
 /* ---- instrumentation ------------------------------------------------------ */
 enum { SGM_FLOW_NUM_STAGES = 3 };   /* propagation, random search, kNN */

@@ -30,7 +30,7 @@ EXPORTS = (
     "sgm_flow_create", "sgm_flow_destroy", "sgm_flow_last_error_string", "sgm_flow_launch_count",
     "sgm_flow", "sgm_flow_field", "sgm_flow_descriptors", "sgm_flow_patch_cost",
     "sgm_flow_knn_init", "sgm_flow_sweep", "sgm_flow_consistency", "sgm_flow_set_timing",
-    "sgm_flow_read_timing", "sgm_densify",
+    "sgm_flow_read_timing", "sgm_densify", "sgm_densify_scratch_bytes",
 )
 
 
@@ -144,7 +144,8 @@ def load(path: str | None = None):
         "sgm_flow_sweep": (st, [P, P, P, I32, I32, I32, I32, I32, ctypes.c_uint64, P, P, P]),
         "sgm_flow_consistency": (st, [P, P, P, P, I32, I32, P, P]),
         "sgm_flow_set_timing": (st, [P, I32]),
-        "sgm_densify": (st, [I32, I32, I32, I32, P, P, P, I32, ctypes.c_float, P, P, P]),
+        "sgm_densify": (st, [I32, I32, I32, I32, P, P, P, I32, ctypes.c_float, P, P, P, I64, P]),
+        "sgm_densify_scratch_bytes": (I64, [I32, I32, I32]),
         "sgm_flow_read_timing": (I32, [P, ctypes.POINTER(ctypes.c_float)]),
     }
     for name, (res, args) in sig.items():

@@ -165,16 +165,21 @@ __global__ void densify_kernel(const DensifyParams p, const int *__restrict__ ro
 
 }  // namespace
 
-cudaError_t launch_densify(const DensifyParams &p, cudaStream_t st) {
+size_t densify_scratch_bytes(int n, int W, int H) {
+    const size_t rown = size_t(n) * H * (W + 1), coln = size_t(n) * W * (H + 1);
+    const size_t npx = size_t(n) * W * H;
+    return sizeof(int) * (rown + coln) + 2 * npx + 16;
+}
+
+cudaError_t launch_densify(const DensifyParams &p, void *scratch_in, cudaStream_t st) {
     if (p.K < 1 || p.K > kDensifyKMax) return cudaErrorInvalidValue;
     cudaError_t e = cudaSuccess;
     if (p.unfilled) e = cudaMemsetAsync(p.unfilled, 0, sizeof(int), st);
-    // prefix counts in stream-ordered scratch
+    // prefix counts + gradient image: caller scratch, else stream-ordered allocation
     const size_t rown = size_t(p.n) * p.H * (p.W + 1), coln = size_t(p.n) * p.W * (p.H + 1);
-    const size_t npx = size_t(p.n) * p.W * p.H;
-    int *scratch = nullptr;
-    if (e == cudaSuccess)
-        e = cudaMallocAsync(reinterpret_cast<void **>(&scratch), sizeof(int) * (rown + coln) + 2 * npx + 16, st);
+    int *scratch = reinterpret_cast<int *>(scratch_in);
+    if (!scratch && e == cudaSuccess)
+        e = cudaMallocAsync(reinterpret_cast<void **>(&scratch), densify_scratch_bytes(p.n, p.W, p.H), st);
     if (e != cudaSuccess) return e;
     int *rowc = scratch, *colc = scratch + rown;
     uint16_t *grad = reinterpret_cast<uint16_t *>(colc + coln);
@@ -189,8 +194,11 @@ cudaError_t launch_densify(const DensifyParams &p, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess) densify_kernel<<<unsigned(g < 1 ? 1 : g), 128, 0, st>>>(p, rowc, colc, grad);
     if (e == cudaSuccess) e = cudaGetLastError();
-    const cudaError_t e2 = cudaFreeAsync(scratch, st);
-    return e != cudaSuccess ? e : e2;
+    if (!scratch_in) {
+        const cudaError_t e2 = cudaFreeAsync(scratch, st);
+        if (e == cudaSuccess) e = e2;
+    }
+    return e;
 }
 
 }  // namespace sgm

@@ -361,18 +361,26 @@ sgm_status sgm_flow(sgm_flow_handle *h, int32_t n, const uint8_t *frames0, const
     return ff_status(e);
 }
 
+int64_t sgm_densify_scratch_bytes(int32_t n, int32_t width, int32_t height) {
+    if (n < 1 || width < 1 || height < 1 || width > 16384 || height > 16384) return -1;
+    return int64_t(sgm::densify_scratch_bytes(n, width, height));
+}
+
 sgm_status sgm_densify(int32_t n, int32_t width, int32_t height, int32_t channels, const float *field,
                        const uint8_t *valid, const uint8_t *guide, int32_t K, float lambda, float *out,
-                       int32_t *unfilled, void *stream) {
+                       int32_t *unfilled, void *scratch, int64_t scratch_bytes, void *stream) {
     if (n < 1 || width < 1 || height < 1 || width > 16384 || height > 16384 || channels < 1 || channels > 4 ||
         !field || !valid || !guide || !out || K < 1 || K > 64 || !(lambda >= 0.f))
         return SGM_ERR_INVALID_ARGUMENT;
     if ((reinterpret_cast<uintptr_t>(field) & 3) || (reinterpret_cast<uintptr_t>(out) & 3))
         return SGM_ERR_INVALID_ARGUMENT;
+    if (scratch && ((reinterpret_cast<uintptr_t>(scratch) & 15) ||
+                    scratch_bytes < int64_t(sgm::densify_scratch_bytes(n, width, height))))
+        return SGM_ERR_INVALID_ARGUMENT;
     sgm::DensifyParams p{};
     p.n = n; p.W = width; p.H = height; p.C = channels; p.K = K; p.lambda = lambda;
     p.field = field; p.valid = valid; p.guide = guide; p.out = out; p.unfilled = unfilled;
-    return ff_status(sgm::launch_densify(p, static_cast<cudaStream_t>(stream)));
+    return ff_status(sgm::launch_densify(p, scratch, static_cast<cudaStream_t>(stream)));
 }
 
 }  // extern "C"

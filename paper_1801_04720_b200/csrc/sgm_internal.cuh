@@ -119,7 +119,8 @@ cudaError_t launch_repitch(const uint8_t *src, uint8_t *dst, int W, long long pi
                            cudaStream_t st);
 cudaError_t launch_combine(const CombineParams &p, cudaStream_t st);
 cudaError_t launch_evaluate(const EvalParams &p, cudaStream_t st);
-cudaError_t launch_densify(const DensifyParams &p, cudaStream_t st);
+cudaError_t launch_densify(const DensifyParams &p, void *scratch, cudaStream_t st);
+size_t densify_scratch_bytes(int n, int W, int H);
 int evaluate_max_blocks();   // scratch rows launch_evaluate may use besides one per quad
 cudaError_t ff_launch_downsample(const uint8_t *src, long long src_stride, int W, int H, uint8_t *dst,
                                  long long dst_stride, int nimg, cudaStream_t st);

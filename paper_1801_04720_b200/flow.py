@@ -122,10 +122,14 @@ class FlowFields:
         return v
 
 
-def densify(field, valid, guide, K=25, lam=1.0, stream=None, count_unfilled=False):
+_densify_scratch = {}
+
+
+def densify(field, valid, guide, K=25, lam=1.0, stream=None, count_unfilled=False, scratch=None):
     """Edge-aware densification (sgm_densify): field float32 [n][H][W][C] (or [H][W][C]),
     valid / guide uint8 [n][H][W] (device).  Returns the dense field (and the number of
-    pixels of images without seeds if asked)."""
+    pixels of images without seeds if asked).  The scratch buffer is cached per shape and
+    device unless one is passed."""
     squeeze = field.dim() == 3
     if squeeze:
         field, valid, guide = field[None], valid[None], guide[None]
@@ -133,7 +137,14 @@ def densify(field, valid, guide, K=25, lam=1.0, stream=None, count_unfilled=Fals
     n, H, W, C = field.shape
     out = torch.empty_like(field)
     cnt = torch.zeros((1,), dtype=torch.int32, device=field.device) if count_unfilled else None
+    nbytes = int(_lib.load().sgm_densify_scratch_bytes(n, W, H))
+    if scratch is None:
+        key = (field.device, n, W, H)
+        scratch = _densify_scratch.get(key)
+        if scratch is None:
+            scratch = torch.empty((nbytes,), dtype=torch.uint8, device=field.device)
+            _densify_scratch[key] = scratch
     _lib.call("sgm_densify", n, W, H, C, _ptr(field), _ptr(valid.contiguous()), _ptr(guide.contiguous()),
-              int(K), float(lam), _ptr(out), _ptr(cnt), _stream(stream))
+              int(K), float(lam), _ptr(out), _ptr(cnt), _ptr(scratch), nbytes, _stream(stream))
     out = out[0] if squeeze else out
     return (out, cnt) if count_unfilled else out
