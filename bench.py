@@ -441,15 +441,17 @@ def main():
         estf = fo["flow"].cpu().numpy()
         fval = fo["valid"].cpu().numpy() > 0
         epe = np.hypot(estf[..., 0] - gtf[..., 0], estf[..., 1] - gtf[..., 1])
-        # roofline of the propagation kernel: the method's work per sweep is two candidate
-        # data terms per pixel, (2r+1)^2 samples x 8 integer ops (4 bilinear multiply-adds,
-        # Q^2 a, subtract, abs, accumulate); the kernel is a latency-bound wavefront
+        # roofline of the propagation kernel (random search fused in): the method's work per
+        # sweep is three candidate data terms per pixel (left/up or right/down + the random
+        # one), (2r+1)^2 samples x 8 integer ops (4 bilinear multiply-adds, Q^2 a, subtract,
+        # abs, accumulate); the kernel is a latency-bound wavefront
         P = ffh.params
         ops = 0.0
         lw, lh = W, H
         for _lvl in range(P.levels):
             for r in (P.patch_radius, P.patch_radius, P.patch_radius + 2):
-                ops += F * lw * lh * P.sweeps * 2 * (2 * r + 1) ** 2 * 8
+                # two propagation candidates + the fused random-search candidate
+                ops += F * lw * lh * P.sweeps * 3 * (2 * r + 1) ** 2 * 8
             lw, lh = (lw + 1) // 2, (lh + 1) // 2
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         peak_ops = 148 * 128 * sm_mhz * 1e6

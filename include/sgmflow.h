@@ -94,10 +94,11 @@ SGM_API sgm_status sgm_densify(int32_t n, int32_t width, int32_t height, int32_t
 SGM_API int64_t sgm_densify_scratch_bytes(int32_t n, int32_t width, int32_t height);
 
 /* ---- instrumentation ------------------------------------------------------ */
-enum { SGM_FLOW_NUM_STAGES = 3 };   /* propagation, random search, kNN */
+enum { SGM_FLOW_NUM_STAGES = 3 };   /* propagation (incl. the fused random search), -, kNN */
 
-/* Enable (1) / disable (0) CUDA-event timing of the propagation, random-search and kNN
- * kernels of every following sgm_flow / sgm_flow_field call (events on the call's stream). */
+/* Enable (1) / disable (0) CUDA-event timing of the propagation kernels (the random search
+ * runs inside them; stage 1 stays 0) and the kNN kernels of every following sgm_flow /
+ * sgm_flow_field call (events on the call's stream). */
 SGM_API sgm_status sgm_flow_set_timing(sgm_flow_handle *h, int32_t enable);
 
 /* Summed kernel time (ms) per stage of the last timed call into ms[SGM_FLOW_NUM_STAGES]

@@ -21,7 +21,8 @@
 //                         global row buffer, both as tagged 64-bit words polled directly (no
 //                         fences); CTAs take tickets so a band only waits for an
 //                         already-running band
-//   ff_search_kernel      the random search after each sweep (thread per pixel, counter RNG)
+//                         the random search after each sweep is fused in: once a row's
+//                         propagation is done its warp searches the row (lane per pixel)
 //   ff_lift_kernel        x2 vectors, nearest-neighbour upsampling, costs recomputed
 //   ff_consistency_kernel two-inverse-field check (thread per pixel)
 #include <cuda_fp16.h>
@@ -567,36 +568,12 @@ __global__ void ff_lift_kernel(FieldSet fs, const int32_t *__restrict__ coarse, 
     }
 }
 
-// random search (FF7, second half): reads only the pixel's own vector
-__global__ void __launch_bounds__(128, 6) ff_search_kernel(FieldSet fs, int sweep, int level, int R0) {
-    const long long per = (long long)fs.W * fs.H, total = per * fs.nfields;
-    const int R = max(R0 >> sweep, 1);
-    const unsigned span = unsigned(2 * R * FQ + 1);
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int f = int(t / per);
-        const long long p = t - f * per;
-        const int y = int(p / fs.W), x = int(p - (long long)y * fs.W);
-        const int kind = fs.kind(f);
-        const uint64_t z = splitmix(fs.sd(kind), level, sweep, x, y);
-        const int fu = fs.flow[2 * t] + int(unsigned(z) % span) - R * FQ;
-        const int fv = fs.flow[2 * t + 1] + int(unsigned(z >> 32) % span) - R * FQ;
-        const uint8_t *src;
-        const uint32_t *dst;
-        fs.images(f, src, dst);
-        const int c = patch_cost_thread(src, dst, fs.W, fs.H, x, y, fu, fv, fs.rad(kind), fs.pen64);
-        if (c < fs.cost[t]) {
-            fs.cost[t] = c;
-            fs.flow[2 * t] = fu;
-            fs.flow[2 * t + 1] = fv;
-        }
-    }
-}
-
 // ------------------------------------------------------------------ propagation (FF7)
 struct PropParams {
     FieldSet fs;
     int sweep;
+    int level;                    // RNG stream of the fused random search
+    int R0;                       // random-search radius of sweep 0 (px); 0 = no search
     int nbands;
     int *ticket;                  // zeroed before the launch
     unsigned long long *hand;     // [nfields][nbands][W] band handoff rows, zeroed before the launch
@@ -760,6 +737,27 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
         }
         hv = make_int2(cu, cv);
         __syncwarp();
+    }
+    // Random search of this row (FF7, second half), fused into the sweep: it reads only each
+    // pixel's own vector after the propagation, and the rows below take this row's
+    // propagation results from the ring / handoff buffer, not from `flow`, so the order of
+    // S:231 (whole sweep, then the search) is kept.  One lane per pixel.
+    if (pp.R0 > 0) {
+        const int R = max(pp.R0 >> pp.sweep, 1);
+        const unsigned span = unsigned(2 * R * FQ + 1);
+        const uint64_t seed = fs.sd(kind);
+        for (int x = lane; x < W; x += 32) {
+            const long long p = (long long)y * W + x;
+            const uint64_t z = splitmix(seed, pp.level, pp.sweep, x, y);
+            const int fu = flow[2 * p] + int(unsigned(z) % span) - R * FQ;
+            const int fv = flow[2 * p + 1] + int(unsigned(z >> 32) % span) - R * FQ;
+            const int c = patch_cost_thread(src, dst, W, H, x, y, fu, fv, r, fs.pen64);
+            if (c < cost[p]) {
+                cost[p] = c;
+                flow[2 * p] = fu;
+                flow[2 * p + 1] = fv;
+            }
+        }
     }
 }
 
@@ -925,16 +923,13 @@ cudaError_t ff_launch_sweep(const FFFields &F, int sweep, int level, int R0, int
     const size_t sm = ff_prop_smem(F.W);
     e = cudaFuncSetAttribute(ff_prop_kernel<kPropNW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     if (e != cudaSuccess) return e;
+    pp.level = level;
+    pp.R0 = R0;                               // the random search runs inside the sweep
     if (timer) timer->begin(0);
     ff_prop_kernel<kPropNW><<<F.nfields * pp.nbands, kPropNW * 32, sm, st>>>(pp);
     if (timer) timer->end();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const long long n = (long long)F.W * F.H * F.nfields;
-    if (timer) timer->begin(1);
-    ff_search_kernel<<<ff_grid(n, 128), 128, 0, st>>>(pp.fs, sweep, level, R0);
-    if (timer) timer->end();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (launches) *launches += 2;
+    if (launches) *launches += 1;
     return cudaSuccess;
 }
 

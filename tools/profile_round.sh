@@ -27,6 +27,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/flow_launches.csv python tools/flow_timing.py 8 3 > gpurun_out/ncu_flow_list.log 2>&1
 echo "ncu flow list exit $?"
 timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"ff_prop_kernel|ff_knn_mma_kernel|ff_search_kernel" -s 30 -c 3 \
+    -k regex:"ff_prop_kernel|ff_knn_mma_kernel" -s 20 -c 3 \
     -o gpurun_out/prof_flow_round python tools/flow_timing.py 8 3 > gpurun_out/ncu_flow_full.log 2>&1
 echo "ncu flow full exit $?"
