@@ -135,8 +135,8 @@ if __name__ == "__main__":
         launches(tag, "flow_launches.csv", f"{tag}_flow_launches.md", "optical-flow kernel launch list (row f2)",
                  "`python tools/flow_timing.py 8 3` (8 Driving pairs, 3 fields each, 3 levels; 8 calls)")
     full(tag, "prof_flow_round.ncu-rep", f"{tag}_flow_ncu.md", "the main optical-flow kernels (row f2)",
-         "`ncu --set full --clock-control none --import-source on -k regex:\"ff_prop_kernel|ff_knn_mma_kernel|"
-         "\" -s 20 -c 3 python tools/flow_timing.py 8 3`", traffic)
+         "`ncu --set full --clock-control none --import-source on -k regex:\"ff_prop_kernel|ff_knn_mma_kernel\" "
+         "-s 20 -c 3 python tools/flow_timing.py 8 3`", traffic)
     json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
     b = os.path.join(OUT, "bench_full.json")
     if os.path.exists(b):
