@@ -330,3 +330,31 @@ def test_invalid_device_arguments(dev):
     with pytest.raises(_lib.SgmError):
         g.census(img)
     g.close()
+
+
+def test_random_small_instances(orc, dev):
+    """SPEC acceptance: 50 random instances up to 16x16x8 -- random size,
+    disparity range, census window and penalties -- with an exact integer match of the
+    aggregated volume S and of the integer disparities of both views."""
+    rng = np.random.default_rng(2024)
+    for it in range(50):
+        W, H = int(rng.integers(1, 17)), int(rng.integers(1, 17))
+        D = int(rng.integers(1, 9))
+        cw, ch = [(3, 3), (5, 5), (3, 1), (1, 3), (7, 5)][it % 5]
+        cmax = cw * ch - 1
+        P1 = int(rng.integers(0, 20))
+        P2 = int(rng.integers(P1, min(255 - cmax, 120) + 1))
+        img = rng.integers(0, 256, size=(H, W)).astype(np.uint8)
+        shift = int(rng.integers(0, 4))
+        L = img
+        R = np.roll(img, -shift, axis=1)
+        g = make_sgm(W, H, D, cw, ch, P1, P2)
+        cl, cr = g.census(g.upload_image(L)), g.census(g.upload_image(R))
+        ocl, ocr = orc.census(L, cw, ch), orc.census(R, cw, ch)
+        for view, s in ((0, -1), (1, +1)):
+            ref, match = (ocl, ocr) if view == 0 else (ocr, ocl)
+            di, ds, C, S = orc.sgm_view(ref, match, D, s, cmax, P1, P2, want_S=True)
+            gS = g.aggregate(cl, cr, view)
+            torch.cuda.synchronize()
+            assert np.array_equal(_np(gS).astype(np.uint32), S), (it, view, W, H, D)
+        g.close()
