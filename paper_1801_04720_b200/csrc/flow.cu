@@ -65,6 +65,33 @@ struct Cand {
     }
 };
 
+// Candidate setup for the warp-cooperative evaluation at pixel (x, y): per-lane sample k is
+// the pixel (x + sdx[k], y + sdy[k]); its B position (bx + sdx[k], by + sdy[k]) is inside
+// iff both unsigned coordinates are <= (ux, uy) (ux = 0 with bx pushed far negative when no
+// column can be inside, W = 1 with a fractional part); offsets are 32-bit.
+struct CandW {
+    int base, bx, by;
+    unsigned ux, uy, wpack;
+    __device__ __forceinline__ CandW(int fu, int fv, int x, int y, int W, int H) {
+        const int fx = fu & 7, fy = fv & 7;
+        wpack = unsigned((FQ - fx) * (FQ - fy)) | (unsigned(fx * (FQ - fy)) << 8) |
+                (unsigned((FQ - fx) * fy) << 16) | (unsigned(fx * fy) << 24);
+        const int ixmax = W - 1 - (fx ? 1 : 0), iymax = H - 1 - (fy ? 1 : 0);
+        bx = ixmax >= 0 ? x + (fu >> 3) : -(1 << 29);
+        by = iymax >= 0 ? y + (fv >> 3) : -(1 << 29);
+        ux = ixmax >= 0 ? unsigned(ixmax) : 0u;
+        uy = iymax >= 0 ? unsigned(iymax) : 0u;
+        base = by * W + bx;
+    }
+    __device__ __forceinline__ int cost(const uint32_t *__restrict__ QB, int dx, int dy, int soff, int a,
+                                        int pen64) const {
+        const bool in = unsigned(bx + dx) <= ux && unsigned(by + dy) <= uy;
+        const unsigned t = __ldg(QB + (in ? base + soff : 0));
+        const int b = int(__dp4a(t, wpack, 0u));
+        return in ? abs(FQ2 * a - b) : pen64;
+    }
+};
+
 // The whole data term by one thread, sample order irrelevant (integers).  The
 // row loop is unrolled over the widest supported patch (15) with a predicate, so the
 // loads of a row's samples are in flight together.
@@ -638,9 +665,12 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
         sdy[k] = q / side - r;
         sdx[k] = q - (q / side) * side - r;
     }
-    long long aoff[NK];                             // A row of each of this lane's samples
+    int aoff[NK], soff[NK];                         // A row / B offset of this lane's samples
 #pragma unroll
-    for (int k = 0; k < NK; ++k) aoff[k] = (long long)clampi(y + sdy[k], 0, H - 1) * W;
+    for (int k = 0; k < NK; ++k) {
+        aoff[k] = clampi(y + sdy[k], 0, H - 1) * W;
+        soff[k] = sdy[k] * W + sdx[k];
+    }
     int2 hv = make_int2(0, 0);                      // vector of the previous pixel in scan order
     unsigned long long hbuf = 0ull;                 // band handoff entries of the chunk (lane l)
     // The incumbents (vector + cost) of 32 positions are loaded per chunk, lane l holding
@@ -696,13 +726,12 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
                 a[k] = __ldg(src + aoff[k] + clampi(x + sdx[k], 0, W - 1));
         }
         if (eh && ev) {                             // both candidates: loads in flight together
-            const Cand C0(hv.x, hv.y, W, H), C1(vv.x, vv.y, W, H);
+            const CandW C0(hv.x, hv.y, x, y, W, H), C1(vv.x, vv.y, x, y, W, H);
             int s0 = 0, s1 = 0;
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
-                const int sx = x + sdx[k], sy = y + sdy[k];
-                const int t0 = C0.cost(dst, W, sx + C0.qx, sy + C0.qy, a[k], fs.pen64);
-                const int t1 = C1.cost(dst, W, sx + C1.qx, sy + C1.qy, a[k], fs.pen64);
+                const int t0 = C0.cost(dst, sdx[k], sdy[k], soff[k], a[k], fs.pen64);
+                const int t1 = C1.cost(dst, sdx[k], sdy[k], soff[k], a[k], fs.pen64);
                 s0 += sok[k] ? t0 : 0;
                 s1 += sok[k] ? t1 : 0;
             }
@@ -712,11 +741,11 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
             if (c1 < cc) { cc = c1; cu = vv.x; cv = vv.y; }
         } else if (eh || ev) {                      // one candidate
             const int2 w = eh ? hv : vv;
-            const Cand C0(w.x, w.y, W, H);
+            const CandW C0(w.x, w.y, x, y, W, H);
             int s0 = 0;
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
-                const int t0 = C0.cost(dst, W, x + sdx[k] + C0.qx, y + sdy[k] + C0.qy, a[k], fs.pen64);
+                const int t0 = C0.cost(dst, sdx[k], sdy[k], soff[k], a[k], fs.pen64);
                 s0 += sok[k] ? t0 : 0;
             }
             const int c0 = int(__reduce_add_sync(0xffffffffu, unsigned(s0)));
