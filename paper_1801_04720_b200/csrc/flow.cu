@@ -59,7 +59,7 @@ struct Cand {
     __device__ __forceinline__ int cost(const uint32_t *__restrict__ QB, int W, int ix, int iy, int a,
                                         int pen64) const {
         const bool in = (ix | iy) >= 0 && ix <= ixmax && iy <= iymax;
-        const unsigned t = __ldg(QB + (in ? (long long)iy * W + ix : 0));
+        const unsigned t = __ldg(QB + (in ? iy * W + ix : 0));   // images < 2^31 pixels
         const int b = int(__dp4a(t, wpack, 0u));
         return in ? abs(FQ2 * a - b) : pen64;
     }
@@ -100,7 +100,7 @@ __device__ __forceinline__ int patch_cost_thread(const uint8_t *__restrict__ A, 
     const Cand c(fu, fv, W, H);
     int s = 0;
     for (int dy = -r; dy <= r; ++dy) {
-        const uint8_t *arow = A + (long long)clampi(y + dy, 0, H - 1) * W;
+        const uint8_t *arow = A + clampi(y + dy, 0, H - 1) * W;
         const int iy = y + dy + c.qy;
 #pragma unroll
         for (int k = 0; k < 15; ++k) {
