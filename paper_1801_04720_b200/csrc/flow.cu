@@ -675,17 +675,17 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
     unsigned long long hbuf = 0ull;                 // band handoff entries of the chunk (lane l)
     // The incumbents (vector + cost) of 32 positions are loaded per chunk, lane l holding
     // position 32c + l, one chunk ahead: no global load latency on the row's chain.
-    auto chunk_px = [&](int i) { return (long long)y * W + (fwd ? i : W - 1 - i); };
+    auto chunk_px = [&](int i) { return y * W + (fwd ? i : W - 1 - i); };   // < 2^31 per field
     int cu_l = 0, cv_l = 0, cc_l = 0, nu_l = 0, nv_l = 0, nc_l = 0;
-    if (lane < W) { const long long q = chunk_px(lane); cu_l = flow[2 * q]; cv_l = flow[2 * q + 1]; cc_l = cost[q]; }
-    if (32 + lane < W) { const long long q = chunk_px(32 + lane); nu_l = flow[2 * q]; nv_l = flow[2 * q + 1]; nc_l = cost[q]; }
+    if (lane < W) { const int q = chunk_px(lane); cu_l = flow[2 * q]; cv_l = flow[2 * q + 1]; cc_l = cost[q]; }
+    if (32 + lane < W) { const int q = chunk_px(32 + lane); nu_l = flow[2 * q]; nv_l = flow[2 * q + 1]; nc_l = cost[q]; }
     for (int i = 0; i < W; ++i) {
         const int x = fwd ? i : W - 1 - i;
-        const long long p = (long long)y * W + x;
+        const int p = y * W + x;
         if ((i & 31) == 0 && i > 0) {               // next chunk: rotate and prefetch
             cu_l = nu_l; cv_l = nv_l; cc_l = nc_l;
             if (i + 32 + lane < W) {
-                const long long q = chunk_px(i + 32 + lane);
+                const int q = chunk_px(i + 32 + lane);
                 nu_l = flow[2 * q]; nv_l = flow[2 * q + 1]; nc_l = cost[q];
             }
         }
@@ -776,7 +776,7 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
         const unsigned span = unsigned(2 * R * FQ + 1);
         const uint64_t seed = fs.sd(kind);
         for (int x = lane; x < W; x += 32) {
-            const long long p = (long long)y * W + x;
+            const int p = y * W + x;
             const uint64_t z = splitmix(seed, pp.level, pp.sweep, x, y);
             const int fu = flow[2 * p] + int(unsigned(z) % span) - R * FQ;
             const int fv = flow[2 * p + 1] + int(unsigned(z >> 32) % span) - R * FQ;
