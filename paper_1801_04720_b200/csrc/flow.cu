@@ -470,16 +470,29 @@ __global__ void __launch_bounds__(128) ff_knn_mma_kernel(const KnnEntry *__restr
             mma_f16(c2, ah, bl0, bl1);              // + sum qh bl
             mma_f16(c2, al, bh0, bh1);              // + sum ql bh
             mma_f16(c3, al, bl0, bl1);              // sum ql bl
+            // fp32 screen of the 4 elements first; the exact path runs only when some lane
+            // of the warp has a survivor (rare once the lists have filled)
+            float df[4];
+            unsigned pass = 0u;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+                const float bnf = sNf[b][cg * 8 + 2 * t + jj];
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const float dotf = fmaf(16384.f, c1[2 * rr + jj], fmaf(128.f, c2[2 * rr + jj], c3[2 * rr + jj]));
+                    df[2 * rr + jj] = fmaf(-2.f, dotf, (rr ? qn1f : qn0f) + bnf);
+                    pass |= (df[2 * rr + jj] <= (rr ? lim1 : lim0) ? 1u : 0u) << (2 * rr + jj);
+                }
+            }
+            if (!__any_sync(0xffffffffu, pass != 0u)) continue;
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) {
                 const int col = cg * 8 + 2 * t + jj;
                 const int idx = base + col;
-                const float bnf = sNf[b][col];
 #pragma unroll
                 for (int rr = 0; rr < 2; ++rr) {
-                    const float dotf = fmaf(16384.f, c1[2 * rr + jj], fmaf(128.f, c2[2 * rr + jj], c3[2 * rr + jj]));
-                    const float df = fmaf(-2.f, dotf, (rr ? qn1f : qn0f) + bnf);
-                    if (df <= (rr ? lim1 : lim0) && idx < n) {
+                    // re-test against the bound as updated by earlier insertions
+                    if (df[2 * rr + jj] <= (rr ? lim1 : lim0) && idx < n) {
                         const long long dot = 16384ll * (long long)c1[2 * rr + jj] +
                                               128ll * (long long)c2[2 * rr + jj] + (long long)c3[2 * rr + jj];
                         const long long d = (rr ? qn1 : qn0) + sN[b][col] - 2 * dot;
