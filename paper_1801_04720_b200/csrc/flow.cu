@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(128) ff_knn_kernel(const int32_t *__restrict__
 // |q|^2 + |b|^2 - 2 q.b in 64-bit integers where needed and keeps a (distance,
 // index)-ordered top-k per query row; the 4 lanes holding a row merge their lists at the
 // end.
-constexpr int kMmaTile = 64;             // database entries per shared-memory tile
+constexpr int kMmaTile = 128;             // database entries per shared-memory tile
 
 // (distance, index)-ordered k-best list in local memory (insertions are rare once it has
 // filled); the caller keeps the admission threshold (k-th entry) in registers.
