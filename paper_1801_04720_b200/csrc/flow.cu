@@ -382,7 +382,9 @@ __device__ __forceinline__ void cp_async16_ff(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-__global__ void __launch_bounds__(128) ff_knn_mma_kernel(const KnnEntry *__restrict__ ent,
+constexpr int kKnnWarps = 4;             // warps (x 16 queries) per block sharing each tile
+
+__global__ void __launch_bounds__(kKnnWarps * 32) ff_knn_mma_kernel(const KnnEntry *__restrict__ ent,
                                                          const long long *__restrict__ norm,
                                                          const float *__restrict__ normf, int n, int n_pad,
                                                          int knn, int32_t *__restrict__ nn) {
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(128) ff_knn_mma_kernel(const KnnEntry *__restr
     const KnnEntry *ed = ent + (long long)(prob ^ 1) * n;
     const long long *nq = norm + (long long)prob * n_pad, *nd = norm + (long long)(prob ^ 1) * n_pad;
     const float *nfd = normf + (long long)(prob ^ 1) * n_pad;
-    const int q0 = (blockIdx.x * 4 + warp) * 16;
+    const int q0 = (blockIdx.x * kKnnWarps + warp) * 16;
     const int r0 = q0 + g, r1 = q0 + g + 8;
     // A fragments (m16n8k16, row-major 16 x 16): a0 = row g, k 2t..2t+1; a1 = row g+8;
     // a2 = row g, k 2t+8..2t+9; a3 = row g+8, k 2t+8..2t+9
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(128) ff_knn_mma_kernel(const KnnEntry *__restr
     const float kMargin = 32768.f;
     const float qn0f = float(qn0), qn1f = float(qn1);
     const int ntiles = (n + kMmaTile - 1) / kMmaTile;
-    const int tq = min(int((long long)blockIdx.x * 64 / kMmaTile), ntiles - 1);
+    const int tq = min(int((long long)blockIdx.x * kKnnWarps * 16 / kMmaTile), ntiles - 1);
     auto tile_of = [&](int it) {
         const int up = ntiles - 1 - tq, dn = tq;
         const int h = (it + 1) / 2;
@@ -912,8 +914,8 @@ cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int wi
         long long *norm = reinterpret_cast<long long *>(ent + total);
         float *normf = reinterpret_cast<float *>(norm + (long long)n_pad * (nprob + (nprob & 1)));
         ff_knn_prep_kernel<<<ff_grid(total, 128), 128, 0, st>>>(desc, n, n_pad, total, ent, norm, normf);
-        dim3 grid((n + 63) / 64, nprob);
-        ff_knn_mma_kernel<<<grid, 128, 0, st>>>(ent, norm, normf, n, n_pad, knn, nn);
+        dim3 grid((n + kKnnWarps * 16 - 1) / (kKnnWarps * 16), nprob);
+        ff_knn_mma_kernel<<<grid, kKnnWarps * 32, 0, st>>>(ent, norm, normf, n, n_pad, knn, nn);
     } else {
         dim3 grid((n + 127) / 128, nprob);
         ff_knn_kernel<<<grid, 128, 0, st>>>(desc, n, knn, nn);
