@@ -645,7 +645,7 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned l
 
 // One row of one field in scan order (the body of ff_prop_kernel); NK = samples per lane
 // ((2r+1)^2 <= 32 NK), so every lane's A and B loads of a pixel are issued together.
-template <int NW, int NK>
+template <int NW, int NK, int RC>   // RC >= 0: the patch radius as a compile-time constant
 __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned long long *sring,
                                          volatile int *sprog, int f, int band, int warp, int lane, int j) {
     const FieldSet &fs = pp.fs;
@@ -656,7 +656,7 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
     const uint32_t *dst;
     fs.images(f, src, dst);
     const int kind = fs.kind(f);
-    const int r = fs.rad(kind), side = 2 * r + 1, ns = side * side;
+    const int r = RC >= 0 ? RC : fs.rad(kind), side = 2 * r + 1, ns = side * side;
     const long long per = (long long)W * H;
     int32_t *flow = fs.flow + 2 * f * per;
     int32_t *cost = fs.cost + f * per;
@@ -824,10 +824,14 @@ __global__ void __launch_bounds__(NW * 32) ff_prop_kernel(const PropParams pp) {
     if (j >= pp.fs.H) return;
     const int r = pp.fs.rad(pp.fs.kind(f));
     const int nk = ((2 * r + 1) * (2 * r + 1) + 31) / 32;
-    if (nk <= 1) prop_row<NW, 1>(pp, sring, sprog, f, band, warp, lane, j);
-    else if (nk <= 3) prop_row<NW, 3>(pp, sring, sprog, f, band, warp, lane, j);
-    else if (nk <= 6) prop_row<NW, 6>(pp, sring, sprog, f, band, warp, lane, j);
-    else prop_row<NW, 8>(pp, sring, sprog, f, band, warp, lane, j);
+    // the default radii (r = 4 and the second inverse field's r + 2 = 6) get sample geometry
+    // fixed at compile time
+    if (r == 4) prop_row<NW, 3, 4>(pp, sring, sprog, f, band, warp, lane, j);
+    else if (r == 6) prop_row<NW, 6, 6>(pp, sring, sprog, f, band, warp, lane, j);
+    else if (nk <= 1) prop_row<NW, 1, -1>(pp, sring, sprog, f, band, warp, lane, j);
+    else if (nk <= 3) prop_row<NW, 3, -1>(pp, sring, sprog, f, band, warp, lane, j);
+    else if (nk <= 6) prop_row<NW, 6, -1>(pp, sring, sprog, f, band, warp, lane, j);
+    else prop_row<NW, 8, -1>(pp, sring, sprog, f, band, warp, lane, j);
 }
 
 // ------------------------------------------------------------------ consistency (FF9)
