@@ -122,11 +122,20 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
 // The bias turns the three min operations per pair of the plain form into two (the +P1
 // of the neighbours is already in their stored value).  A path start is the vector P1
 // (L = 0, m = 0), which returns Lb' = C + P1.
-//   sel_up / sel_dn: PRMT selectors building the d-1 / d+1 neighbour pairs (per lane).
+//
+// Folded disparity layout: register r of lane l holds the pair k = R*l + r, i.e. the
+// disparities (k, Dp-1-k) in its (low, high) halves.  The d-1 / d+1 neighbours of both
+// halves of pair k are then the halves of pairs k-1 and k+1, aligned: no byte permutes,
+// one SHFL each way per path.  Two lanes need care:
+//   * pair 0 (lane 0, reg 0) has no pair -1 (d = 0 has no d-1, d = Dp-1 no d+1); the
+//     clamped SHFL returns the lane's own reg R-1, which is pair 1 -- a duplicate of the
+//     other neighbour, hence harmless (G7) -- for R <= 2; for R > 2 it is forced to 0xFFFF.
+//   * pair Dp/2-1 (lane 31, reg R-1) is the fold (Dp/2-1, Dp/2): its "pair k+1" is itself
+//     with the halves swapped -- one PRMT with a per-lane selector (sel_fold).
 template <int R>
 __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uint32_t (&C)[R],
                                             uint32_t (&out)[R], uint32_t negp1x2, uint32_t p2mp1x2,
-                                            uint32_t twop1x2, uint32_t sel_up, uint32_t sel_dn) {
+                                            uint32_t twop1x2, uint32_t sel_fold, uint32_t ff_lane0) {
     // mb = min_k Lb(p - r, k): min over the lane's pairs, then over the two halves (the
     // high half is brought down with IMAD.HI on the FMA pipe), then over the warp
     uint32_t v = prev[0];
@@ -136,18 +145,14 @@ __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uin
     const uint32_t mb = __reduce_min_sync(0xffffffffu, v);
     const uint32_t mP2 = imad(mb, 0x10001u, p2mp1x2);  // m + P2 = mb - P1 + P2, both halves
     const uint32_t K = imad(mb, 0xFFFEFFFFu, twop1x2); // 2 P1 - mb in both halves (mod 2^32)
-    // neighbours d-1 / d+1
-    const uint32_t up = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
-    const uint32_t dn = __shfl_down_sync(0xffffffffu, prev[0], 1);
-    uint32_t nb[R + 1];
-    nb[0] = __byte_perm(up, prev[0], sel_up);
-#pragma unroll
-    for (int r = 1; r < R; ++r) nb[r] = __byte_perm(prev[r - 1], prev[r], 0x5432);
-    nb[R] = __byte_perm(prev[R - 1], dn, sel_dn);
+    // neighbour pairs k-1 (of reg 0) and k+1 (of reg R-1)
+    uint32_t up = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
+    if (R > 2) up |= ff_lane0;
+    const uint32_t dn = __byte_perm(__shfl_down_sync(0xffffffffu, prev[0], 1), prev[R - 1], sel_fold);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t centre = __viaddmin_u16x2(prev[r], negp1x2, mP2);   // min(L(d), m + P2)
-        const uint32_t t = __vimin3_u16x2(nb[r], nb[r + 1], centre);
+        const uint32_t t = __vimin3_u16x2(r == 0 ? up : prev[r - 1], r == R - 1 ? dn : prev[r + 1], centre);
         // C + t - m + P1: exact mod 2^32, every half's result lies in [P1, 2^16)
         out[r] = t + C[r] + K;
     }
@@ -310,21 +315,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     const uint32_t p2mp1x2 = uint32_t(p.P2 - p.P1) * 0x10001u;                  // P2 - P1
     const uint32_t twop1x2 = 2u * p1x2;
     const uint32_t negb4 = 0u - 4u * p1x2;            // removes the 4 path biases from S
-    const int dbase = CPL * lane;
+    const int dbase = CPL * lane;                  // the lane's u16 offset inside a vector
+    // folded layout (path_update): register r holds disparities dlo + r (low half) and
+    // dhi - r (high half)
+    const int dlo = R * lane, dhi = DP - 1 - R * lane;
     constexpr bool has_pad = PAD;                  // D < Dp (template: no padding work otherwise)
-    // PRMT selectors for the d-1 / d+1 neighbour pairs: at d = 0 (lane 0) the missing d-1
-    // candidate is replaced by the d+1 one (min(L(1), L(1)) == min over existing terms,
-    // G7) and symmetrically at d = Dp-1 (lane 31).
-    const uint32_t sel_up = lane == 0 ? 0x5476u : 0x5432u;
-    const uint32_t sel_dn = lane == 31 ? 0x1032u : 0x5432u;
+    const uint32_t sel_fold = lane == 31 ? 0x5476u : 0x3210u;    // swap the halves at the fold
+    const uint32_t ff_lane0 = lane == 0 ? 0xffffffffu : 0u;      // pair -1 does not exist
     uint32_t pad[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        pad[r] = (dbase + 2 * r >= p.D ? 0x1000u : 0u) | (dbase + 2 * r + 1 >= p.D ? 0x10000000u : 0u);
+        pad[r] = (dlo + r >= p.D ? 0x1000u : 0u) | (dhi - r >= p.D ? 0x10000000u : 0u);
     }
     uint32_t dcode[R];   // bytes: d_lo, d_hi, 0, 0 (WTA keys)
 #pragma unroll
-    for (int r = 0; r < R; ++r) dcode[r] = uint32_t(dbase + 2 * r) | (uint32_t(dbase + 2 * r + 1) << 8);
+    for (int r = 0; r < R; ++r) dcode[r] = uint32_t(dlo + r) | (uint32_t(dhi - r) << 8);
 
     // Ring layout (consumer-centric): slot s of a warp's ring holds, for the position q
     // with q & (kRing-1) == s, the three row-above vectors the consumer needs at q:
@@ -404,9 +409,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
 #pragma unroll
     for (int r = 0; r < R; ++r) Lh[r] = p1x2;                // path start (biased zero)
     using CW = typename std::conditional<C64, uint64_t, uint32_t>::type;
-    CW win[CPL];
+    // census windows of the two halves' disparity chains: lw[] holds census_match(x - d)
+    // for d = dlo + r, hw[] for d = dhi - r (rotating slot indices, see the slide below)
+    CW lw[R], hw[R];
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) win[k] = 0;
+    for (int k = 0; k < R; ++k) { lw[k] = 0; hw[k] = 0; }
     // BWD: S_fwd register prefetch PF positions ahead (slot = position mod PF must be a
     // compile-time index, so PF divides the unroll CPL)
     constexpr int PF = (CPL == 4) ? 4 : 2;
@@ -474,18 +481,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                 }
                 __syncwarp();
             }
-            // --- slide the census window by one position
+            // --- slide the census windows by one position: cell d takes cell d-1's value.
+            // Low chain (d = dlo + r, logical r in slot (r - ph) mod R): enters at r = 0
+            // from lane l-1 (lane 0: the fresh census), leaves at r = R-1.  High chain
+            // (d = dhi - r, logical r in slot (r + ph) mod R): enters at r = R-1 from lane
+            // l+1 (lane 31: its own low chain's outgoing d = Dp/2-1), leaves at r = 0.
             if (!BWD) {
                 const uint64_t fresh = cfresh[i & 63];
-                if (!BWD) {
-                    const int q = (CPL - ph) % CPL;       // outgoing logical CPL-1
-                    CW v = __shfl_up_sync(0xffffffffu, win[q], 1);
-                    win[q] = lane == 0 ? CW(fresh) : v;
-                } else {
-                    const int q = (ph - 1 + CPL) % CPL;   // outgoing logical 0
-                    CW v = __shfl_down_sync(0xffffffffu, win[q], 1);
-                    win[q] = lane == 31 ? CW(fresh) : v;
-                }
+                const int ql = (2 * R - ph) % R;
+                const int qh = (ph + R - 1) % R;
+                const CW out_lo = lw[ql];
+                const CW vl = __shfl_up_sync(0xffffffffu, out_lo, 1);
+                const CW vh = __shfl_down_sync(0xffffffffu, hw[qh], 1);
+                lw[ql] = lane == 0 ? CW(fresh) : vl;
+                hw[qh] = lane == 31 ? out_lo : vh;
             }
             // --- matching cost C(x', d) for the lane's CPL cells.  The forward sweep
             // computes it from the census window; the backward sweep unpacks it from the
@@ -506,21 +515,24 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                 sfwd_ptr += sstep;
             } else {
                 const uint64_t rv = cref[i & 63];
-                uint32_t c[CPL];
+                uint32_t c[CPL];                           // c[2r]: d = dlo + r, c[2r+1]: d = dhi - r
 #pragma unroll
                 for (int jj = 0; jj < CPL; ++jj) {
-                    const int phys = BWD ? (jj + ph) % CPL : (jj - ph + CPL) % CPL;
+                    const int r = jj >> 1;
+                    const CW w = (jj & 1) ? hw[(r + ph) % R] : lw[(r - ph + 2 * R) % R];
                     if (C64) {
-                        const uint64_t x = rv ^ uint64_t(win[phys]);
+                        const uint64_t x = rv ^ uint64_t(w);
                         c[jj] = imad(uint32_t(__popc(uint32_t(x))), one, uint32_t(__popc(uint32_t(x >> 32))));
                     } else {
-                        c[jj] = __popc(uint32_t(rv) ^ uint32_t(win[phys]));
+                        c[jj] = __popc(uint32_t(rv) ^ uint32_t(w));
                     }
                 }
                 if (xv < Dm1) {                            // border: x' - d < 0 -> C_max
 #pragma unroll
-                    for (int jj = 0; jj < CPL; ++jj)
-                        if (dbase + jj > xv) c[jj] = uint32_t(p.cmax);
+                    for (int r = 0; r < R; ++r) {
+                        if (dlo + r > xv) c[2 * r] = uint32_t(p.cmax);
+                        if (dhi - r > xv) c[2 * r + 1] = uint32_t(p.cmax);
+                    }
                 }
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
@@ -543,14 +555,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             uint32_t S[R];
             {
                 uint32_t nL[R];
-                path_update<R>(Lh, C, nL, negp1x2, p2mp1x2, twop1x2, sel_up, sel_dn);
+                path_update<R>(Lh, C, nL, negp1x2, p2mp1x2, twop1x2, sel_fold, ff_lane0);
 #pragma unroll
                 for (int r = 0; r < R; ++r) { Lh[r] = nL[r]; S[r] = nL[r]; }
             }
             uint32_t nv[3][R];
 #pragma unroll
             for (int v = 0; v < 3; ++v)
-                path_update<R>(pv[v], C, nv[v], negp1x2, p2mp1x2, twop1x2, sel_up, sel_dn);
+                path_update<R>(pv[v], C, nv[v], negp1x2, p2mp1x2, twop1x2, sel_fold, ff_lane0);
             // S = sum of the four unbiased path costs: the -4 P1 rides in IADD3's third slot
 #pragma unroll
             for (int r = 0; r < R; ++r) S[r] = (S[r] + nv[0][r] + nv[1][r]) + (nv[2][r] + negb4);
@@ -601,10 +613,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                     const int x = X(xv);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int d0 = dbase + 2 * r;
                         uint16_t *o = p.sout + ((long long)y * W + x) * p.D;
-                        if (d0 < p.D) o[d0] = uint16_t(St[r] & 0xffffu);
-                        if (d0 + 1 < p.D) o[d0 + 1] = uint16_t(St[r] >> 16);
+                        if (dlo + r < p.D) o[dlo + r] = uint16_t(St[r] & 0xffffu);
+                        if (dhi - r < p.D) o[dhi - r] = uint16_t(St[r] >> 16);
                     }
                 }
                 if (do_wta) {
@@ -619,7 +630,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                     const uint32_t bkey = __reduce_min_sync(0xffffffffu, best);
                     const int dstar = int(bkey & 0xffu);
                     __syncwarp();                                // previous reads of wta done
-                    VecIO<R>::st(wta + dbase, St);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {           // natural disparity order
+                        wta[dlo + r] = uint16_t(St[r]);
+                        wta[dhi - r] = uint16_t(__umulhi(St[r], 0x10000u));
+                    }
                     __syncwarp();
                     const uint32_t sa = wta[max(dstar - 1, 0)];
                     const uint32_t sc = wta[min(dstar + 1, DP - 1)];
