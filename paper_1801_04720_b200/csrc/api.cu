@@ -25,7 +25,8 @@ struct sgm_handle {
     int max_views = 0;
     // scratch (device)
     uint64_t *census = nullptr;     // [4*max_batch][H][W]
-    uint16_t *sfwd = nullptr;       // [4*max_batch][H][W][Dp]
+    uint16_t *sfwd = nullptr;       // [4*max_batch][H][W][Dp], after a front guard
+    uint16_t *sfwd_alloc = nullptr; // the allocation: kSfwdGuard positions of Dp, then sfwd
     int16_t *dint = nullptr;        // [4*max_batch][H][W]
     float *dsub = nullptr;          // [4*max_batch][H][W]
     int16_t *lr_int = nullptr;      // [2*max_batch][H][W]
@@ -77,7 +78,7 @@ cudaError_t dalloc(T **p, size_t count) {
 }
 
 void free_all(sgm_handle *h) {
-    void *ptrs[] = {h->census, h->sfwd, h->dint, h->dsub, h->lr_int, h->lr_sub, h->lr_valid,
+    void *ptrs[] = {h->census, h->sfwd_alloc, h->dint, h->dsub, h->lr_int, h->lr_sub, h->lr_valid,
                     h->gbuf, h->sync, h->sync_host, h->eval_part};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -174,7 +175,11 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     const size_t nv = size_t(h->max_views), npx = size_t(h->npx);
     h->stage_pitch = ((long long)W + 15) / 16 * 16;
     if (e == cudaSuccess) e = dalloc(&h->census, nv * npx);
-    if (e == cudaSuccess) e = dalloc(&h->sfwd, nv * npx * size_t(h->dp));
+    // the backward sweep prefetches S_fwd a few positions ahead without clamping: the
+    // first row's prefetch reads into the front guard
+    constexpr size_t kSfwdGuard = 16;
+    if (e == cudaSuccess) e = dalloc(&h->sfwd_alloc, (nv * npx + kSfwdGuard) * size_t(h->dp));
+    if (e == cudaSuccess) h->sfwd = h->sfwd_alloc + kSfwdGuard * size_t(h->dp);
     if (e == cudaSuccess) e = dalloc(&h->dint, nv * npx);
     if (e == cudaSuccess) e = dalloc(&h->dsub, nv * npx);
     if (e == cudaSuccess) e = dalloc(&h->lr_int, nv / 2 * npx);

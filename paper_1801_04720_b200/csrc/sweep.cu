@@ -181,7 +181,7 @@ struct Sweep {
         b += size_t(RING0) * VEC * 2;               // band input ring
         b += size_t(NW) * 2 * CEN * 8;              // census prefetch (ref, fresh)
         if (BWD) {
-            b += size_t(NW) * DP * 2;               // WTA scratch
+            b += size_t(NW) * (DP + 4) * 2;         // WTA scratch (S(d) at index d + 2)
         }
         b += size_t(2) * NW * RG * 8;               // full / empty mbarriers
         b += size_t(2) * kPubDepth * 8;             // publisher mbarriers
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     constexpr int RING0 = SW::RING0;
     uint64_t *cbuf = reinterpret_cast<uint64_t *>(in0 + size_t(RING0) * VEC);
     uint16_t *wsc = reinterpret_cast<uint16_t *>(cbuf + size_t(NW) * 2 * SW::CEN);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(wsc + (BWD ? size_t(NW) * DP : 0));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(wsc + (BWD ? size_t(NW) * (DP + 4) : 0));
     // full[w][s]: slot s of warp w's ring holds complete data (32 producer lanes arrive)
     // empty[w][s]: the consumer (warp w+1) is done with slot s (32 consumer lanes arrive)
     // pub_full[k] / pub_empty[k]: band producer -> publisher warp handoff (kPubDepth deep)
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     uint64_t *src_empty = bars + size_t(NW + warp - 1) * RG;
     uint64_t *cref = cbuf + size_t(warp) * 128;
     uint64_t *cfresh = cref + 64;
-    uint16_t *wta = wsc + size_t(warp) * DP;
+    uint16_t *wta = wsc + size_t(warp) * (DP + 4);
 
     // band handoff (gbuf row has the same consumer-centric layout per position)
     const int nb_id = view * p.nbands + band;
@@ -509,9 +509,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                     Sf[r] = (pf[slot][r] >> 6) & 0x03FF03FFu;
                     C[r] = PAD ? craw[r] + pad[r] : craw[r];
                 }
-                // unconditional load (clamped to the last position): a predicated load would
-                // make the compiler copy the result into the slot at once and stall on it
-                VecIO<R>::ld(sfwd_ptr + (i + PF < W ? PF : W - 1 - i) * sstep, pf[slot]);
+                // unconditional load: a predicated load would make the compiler copy the
+                // result into the slot at once and stall on it.  Past the row's end it reads
+                // the row before (or the allocation's front guard); the value is never used.
+                VecIO<R>::ld(sfwd_ptr + PF * sstep, pf[slot]);
                 sfwd_ptr += sstep;
             } else {
                 const uint64_t rv = cref[i & 63];
@@ -632,12 +633,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                     __syncwarp();                                // previous reads of wta done
 #pragma unroll
                     for (int r = 0; r < R; ++r) {           // natural disparity order
-                        wta[dlo + r] = uint16_t(St[r]);
-                        wta[dhi - r] = uint16_t(__umulhi(St[r], 0x10000u));
+                        wta[2 + dlo + r] = uint16_t(St[r]);
+                        wta[2 + dhi - r] = uint16_t(__umulhi(St[r], 0x10000u));
                     }
                     __syncwarp();
-                    const uint32_t sa = wta[max(dstar - 1, 0)];
-                    const uint32_t sc = wta[min(dstar + 1, DP - 1)];
+                    // S(d*-1), S(d*+1): one guard entry each side, no clamping (unused at
+                    // d* = 0 / Dp-1)
+                    const uint32_t sa = wta[dstar + 1];
+                    const uint32_t sc = wta[dstar + 3];
                     const int sl = i & 31;
                     if (lane == sl) { rec_key = bkey; rec_ac = sa | (sc << 16); }
                     // every 32 positions each lane finishes one pixel: the parabola
