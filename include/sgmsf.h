@@ -271,13 +271,15 @@ SGM_API const char *sgm_stage_name(int32_t stage);
 SGM_API int64_t sgm_launch_count(sgm_handle *h);
 
 /* Internal geometry, for tests and roofline accounting: padded disparity
- * count Dp (multiple of 64), cells per lane, warps per CTA of the sweeps,
- * rows per band. Any pointer may be NULL. */
+ * count Dp (multiple of 64), cells per lane, compute warps per CTA of the
+ * sweeps (the maximum band height, 17), and the band height chosen for a full
+ * batch (each call picks bands of 10..17 rows so that its CTA count fills
+ * whole waves of the device's SMs). Any pointer may be NULL. */
 SGM_API sgm_status sgm_get_geometry(sgm_handle *h, int32_t *dp, int32_t *cells_per_lane,
                             int32_t *sweep_warps, int32_t *band_rows);
 
 /* Debugging aid: when `trace` (device memory, >= 4 * (sweep_warps + 1) * 4 * max_batch *
- * ceil(H / band_rows) uint64) is non-NULL, every sweep CTA warp writes {start ns, end ns,
+ * ceil(H / 10) uint64) is non-NULL, every sweep CTA warp writes {start ns, end ns,
  * SM id, 0} of its row loop at index (ticket * (sweep_warps + 1) + warp) * 4 (the last
  * launch wins).  NULL disables it (default). */
 SGM_API sgm_status sgm_debug_set_trace(sgm_handle *h, uint64_t *trace);

@@ -18,7 +18,9 @@ int sweep_warps_for(int cpl);
 struct sgm_handle {
     sgm_params prm;
     int device = 0;
-    int cpl = 0, dp = 0, nw = 0, nbands = 0;
+    int cpl = 0, dp = 0, nw = 0;
+    int nbands = 0;                 // allocated bands per view: ceil(H / kBandRowsMin)
+    int nsm = 148;                  // SMs of the device (band_geometry)
     bool c64 = false;
     int cmax = 0;
     long long npx = 0;
@@ -32,7 +34,7 @@ struct sgm_handle {
     int16_t *lr_int = nullptr;      // [2*max_batch][H][W]
     float *lr_sub = nullptr;
     uint8_t *lr_valid = nullptr;
-    uint16_t *gbuf = nullptr;       // [4*max_batch][nbands][W][3][Dp]
+    uint16_t *gbuf = nullptr;       // [4*max_batch][bands of the call][W][3][Dp] (<= nbands)
     int *sync = nullptr;            // [1 + 4*max_batch*nbands]
     unsigned *eval_part = nullptr;  // [evaluate_max_blocks() + max_batch][12] + ticket
     // staging for the _host entry point (device): two slots so that back-to-back calls
@@ -96,18 +98,58 @@ void free_all(sgm_handle *h) {
         if (e) cudaEventDestroy(e);
 }
 
+// Band height of the sweeps for a call with `nviews` views (one CTA per band, one CTA per
+// SM).  Rule fitted to measurements on this B200 (K2):
+//  * with >= 2 waves of 16-row bands, 16 rows (4 compute warps per SM sub-partition) are
+//    the most efficient; 17 rows (18 warps: 5 compute warps on one sub-partition) only pay
+//    when they save a whole wave (32 Driving views, H = 375: 23 bands of 16-17 rows = 736
+//    CTAs = 5 waves instead of 24 x 16 = 768 CTAs = 6; 7.30 -> 7.17 ms per step);
+//  * below 2 waves the SMs are under-filled and shorter bands spread the work: the height
+//    in [kBandRowsMin, 16] minimising ceil(CTAs / SMs) * T(h), T(h) = h/16 (1 + 0.012
+//    (16 - h)) (fewer warps hide less latency), is taken (one Driving quad: 35 bands of
+//    10-11 rows on 140 SMs instead of 24 x 16 on 96: 3.46 -> 3.31 ms).
+// Rows are spread evenly over the bands (heights differ by <= 1).  SGM_BAND_ROWS
+// (environment, experiments) forces the height.
+void band_geometry(int H, int nviews, int nsm, int *nbands, int *q, int *r) {
+    static const int forced = [] {
+        const char *e = getenv("SGM_BAND_ROWS");
+        return e ? atoi(e) : 0;
+    }();
+    auto bands = [&](int rows) { return (H + rows - 1) / rows; };
+    auto waves = [&](int nb) { return ((long long)nviews * nb + nsm - 1) / nsm; };
+    int nb;
+    if (forced >= sgm::kBandRowsMin && forced <= sgm::kBandRowsMax) {
+        nb = bands(forced);
+    } else if ((long long)nviews * bands(16) >= 2LL * nsm) {
+        nb = waves(bands(17)) < waves(bands(16)) ? bands(17) : bands(16);
+    } else {
+        nb = bands(16);
+        double best = -1.0;
+        for (int rows = 16; rows >= sgm::kBandRowsMin; --rows) {
+            const int n = bands(rows), bq = H / n, br = H % n;
+            auto t = [](int h) { return h / 16.0 * (1.0 + 0.012 * (16 - h)); };
+            const double cost = double(waves(n)) * ((n - br) * t(bq) + br * t(bq + 1)) / n;
+            if (best < 0 || cost < best - 1e-9) { best = cost; nb = n; }
+        }
+    }
+    *nbands = nb;
+    *q = H / nb;
+    *r = H % nb;
+}
+
 sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int *sync = nullptr) {
     sgm::SweepParams p{};
     const long long v0 = 0;
     p.W = h->prm.width; p.H = h->prm.height; p.D = h->prm.num_disp; p.Dp = h->dp;
     p.P1 = h->prm.p1; p.P2 = h->prm.p2; p.cmax = h->cmax;
-    p.nviews = nviews; p.nbands = h->nbands;
+    p.nviews = nviews;
+    band_geometry(p.H, nviews, h->nsm, &p.nbands, &p.band_q, &p.band_r);
     p.cen = h->census + v0 * h->npx; p.cen_img_stride = h->npx;
     p.explicit_mode = 0;
     p.sfwd = h->sfwd + v0 * h->npx * h->dp; p.sfwd_view_stride = h->npx * h->dp;
     p.dint = h->dint + v0 * h->npx; p.dsub = h->dsub + v0 * h->npx; p.disp_view_stride = h->npx;
     p.sout = nullptr;
-    p.gbuf = h->gbuf + v0 * h->nbands * (long long)h->prm.width * 3 * h->dp;
+    p.gbuf = h->gbuf + v0 * p.nbands * (long long)h->prm.width * 3 * h->dp;
     if (!sync) sync = h->sync;
     p.progress = sync + 1; p.ticket = sync;
     p.trace = h->trace;
@@ -167,11 +209,12 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     h->cpl = 2 * ((D + 63) / 64);
     h->dp = 32 * h->cpl;
     h->nw = sgm::sweep_warps_for(h->cpl);
-    h->nbands = (H + h->nw - 1) / h->nw;
+    h->nbands = (H + sgm::kBandRowsMin - 1) / sgm::kBandRowsMin;
     h->npx = (long long)W * H;
     h->max_views = 4 * p->max_batch;
 
     cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, device);
     const size_t nv = size_t(h->max_views), npx = size_t(h->npx);
     h->stage_pitch = ((long long)W + 15) / 16 * 16;
     if (e == cudaSuccess) e = dalloc(&h->census, nv * npx);
@@ -237,7 +280,11 @@ sgm_status sgm_get_geometry(sgm_handle *h, int32_t *dp, int32_t *cells_per_lane,
     if (dp) *dp = h->dp;
     if (cells_per_lane) *cells_per_lane = h->cpl;
     if (sweep_warps) *sweep_warps = h->nw;
-    if (band_rows) *band_rows = h->nw;
+    if (band_rows) {                // band height chosen for a full batch (4 * max_batch views)
+        int nb, q, r;
+        band_geometry(h->prm.height, h->max_views, h->nsm, &nb, &q, &r);
+        *band_rows = q + (r > 0);
+    }
     return SGM_OK;
 }
 

@@ -15,6 +15,11 @@ constexpr int kRing0 = 16;      // band-input ring of warp 0 (positions)
 constexpr int kLook = 8;        // band-input prefetch distance (positions)
 constexpr int kPublish = 8;     // band-output progress publication granularity (positions)
 constexpr int kPubDepth = 4;    // producer -> publisher-warp handoff depth (groups)
+// SGM sweep bands: a CTA carries one band of up to kBandRowsMax rows (one compute warp per
+// row); the host picks the band height per call in [kBandRowsMin, kBandRowsMax] so that
+// the CTA count fills whole waves of the SMs (band_geometry in api.cu)
+constexpr int kBandRowsMax = 17;
+constexpr int kBandRowsMin = 10;
 constexpr uint32_t kSent = 0x7FFF7FFFu;   // "no neighbour" path cost (both halves)
 constexpr uint32_t kPadCost = 0x10001000u; // OR-ed into padded disparities d >= D
 
@@ -23,6 +28,7 @@ struct SweepParams {
     int W, H, D, Dp;
     int P1, P2, cmax;
     int nviews, nbands;
+    int band_q, band_r;       // band b has band_q + (b < band_r) rows, from row b*band_q + min(b, band_r)
     // census images [img][H][W]; batch views: view v -> pair v/2, side v%2
     //   side 0: ref = img 2*(v/2), match = img 2*(v/2)+1, mirror 0 (left reference)
     //   side 1: ref = img 2*(v/2)+1, match = img 2*(v/2), mirror 1 (right reference)

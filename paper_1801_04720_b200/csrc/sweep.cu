@@ -177,7 +177,7 @@ struct Sweep {
 
     static constexpr size_t smem_bytes() {
         size_t b = 0;
-        b += size_t(NW) * RS * VEC * 2;             // ring
+        b += size_t(NW - 1) * RS * VEC * 2;         // ring (the band's last row writes none)
         b += size_t(RING0) * VEC * 2;               // band input ring
         b += size_t(NW) * 2 * CEN * 8;              // census prefetch (ref, fresh)
         if (BWD) {
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint16_t *ring = reinterpret_cast<uint16_t *>(smem_raw);
-    uint16_t *in0 = ring + size_t(NW) * RS * VEC;
+    uint16_t *in0 = ring + size_t(NW - 1) * RS * VEC;
     constexpr int RING0 = SW::RING0;
     uint64_t *cbuf = reinterpret_cast<uint64_t *>(in0 + size_t(RING0) * VEC);
     uint16_t *wsc = reinterpret_cast<uint16_t *>(cbuf + size_t(NW) * 2 * SW::CEN);
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     // L = C, i.e. every slot nobody writes acts as a path start.
     {
         uint4 *z = reinterpret_cast<uint4 *>(smem_raw);
-        const int n16 = int((size_t(NW) * RS + RING0) * VEC * 2 / 16);
+        const int n16 = int((size_t(NW - 1) * RS + RING0) * VEC * 2 / 16);
         const uint32_t ps = uint32_t(p.P1) * 0x10001u;     // biased path-start vector
         for (int k = threadIdx.x; k < n16; k += (NW + 1) * 32) z[k] = make_uint4(ps, ps, ps, ps);
     }
@@ -281,9 +281,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
         }
         return;
     }
-    const int j = band * NW + warp;                 // iteration row
-    if (j >= H) return;                             // rows past the image (last band)
-    const bool has_row_below = (warp < NW - 1) && (j + 1 < H) && !(p.debug_flags & 1);
+    // this band's rows (runtime height <= NW, see band_geometry in api.cu)
+    const int hb = p.band_q + (band < p.band_r ? 1 : 0);
+    const int j = band * p.band_q + min(band, p.band_r) + warp;   // iteration row
+    if (warp >= hb) return;                         // rows past the band
+    const bool has_row_below = (warp < hb - 1) && !(p.debug_flags & 1);
     const int y = BWD ? (H - 1 - j) : j;
 
     const uint64_t *ref, *match;
@@ -350,7 +352,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     // band handoff (gbuf row has the same consumer-centric layout per position)
     const int nb_id = view * p.nbands + band;
     const bool has_consumer = band + 1 < p.nbands;
-    const bool is_producer = (warp == NW - 1) && has_consumer && !(p.debug_flags & 3);
+    const bool is_producer = (warp == hb - 1) && has_consumer && !(p.debug_flags & 3);
     uint16_t *gout = p.gbuf + (long long)nb_id * W * VEC + dbase;
     const uint16_t *gin = p.gbuf + (long long)(nb_id - 1) * W * VEC;
     const int *prog_in = p.progress + (nb_id - 1);
@@ -719,7 +721,7 @@ cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cud
 
 }  // namespace
 
-int sweep_warps_for(int cpl) { (void)cpl; return 16; }
+int sweep_warps_for(int cpl) { (void)cpl; return kBandRowsMax; }
 
 cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool debug_s,
                           cudaStream_t st, cudaEvent_t mid_ev_a, cudaEvent_t mid_ev_b,
@@ -731,9 +733,9 @@ cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool 
 #define SGM_CASE(CPL_, C64_)                                                                   \
     if (cpl == CPL_ && c64 == C64_) {                                                          \
         if (p.D < 32 * CPL_)                                                                   \
-            return launch_pair<CPL_, C64_, 16, true>(                        \
+            return launch_pair<CPL_, C64_, kBandRowsMax, true>(                        \
                 p, debug_s, st, mid_ev_a, mid_ev_b, launches, sync_buf, sync_bytes);           \
-        return launch_pair<CPL_, C64_, 16, false>(                           \
+        return launch_pair<CPL_, C64_, kBandRowsMax, false>(                           \
             p, debug_s, st, mid_ev_a, mid_ev_b, launches, sync_buf, sync_bytes);               \
     }
     SGM_CASE(2, false) SGM_CASE(2, true) SGM_CASE(4, false) SGM_CASE(4, true)

@@ -15,9 +15,10 @@ cfg = synth.CONFIGS["batch"]
 g = SGM.from_config(cfg, max_batch=F)
 geo = g.geometry()
 nw = geo["sweep_warps"]
-nb = (cfg.H + nw - 1) // nw
+nb = (cfg.H + geo["band_rows"] - 1) // geo["band_rows"]
 ncta = 4 * F * nb
-tr = torch.zeros(ncta * (nw + 1) * 4, dtype=torch.int64, device="cuda")
+print("band rows", geo["band_rows"], "bands", nb)
+tr = torch.zeros(4 * F * ((cfg.H + 9) // 10) * (nw + 1) * 4, dtype=torch.int64, device="cuda")
 g.lib.sgm_debug_set_trace(g.h, ctypes.c_void_p(tr.data_ptr()))
 quads = [synth.make_quad(cfg, i) for i in range(F)]
 imgs, flow = stack_quads(quads, g.pitch, torch.device("cuda"))
@@ -27,7 +28,7 @@ out = g.alloc_outputs(F)
 for _ in range(3):
     g.scene_flow(imgs, flow, cam, out)
 torch.cuda.synchronize()
-t = tr.cpu().numpy().reshape(ncta, nw + 1, 4).astype(np.float64)
+t = tr.cpu().numpy()[:ncta * (nw + 1) * 4].reshape(ncta, nw + 1, 4).astype(np.float64)
 # the backward sweep ran last: its timeline is in the buffer
 t0 = t[:, :nw, 0][t[:, :nw, 0] > 0].min()
 st = (t[:, :nw, 0] - t0) / 1e3
