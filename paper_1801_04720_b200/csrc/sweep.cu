@@ -16,20 +16,22 @@
 //    written once, in 64*CPL-byte coalesced chunks.  The backward sweep walks
 //    bottom->top, right->left, evaluates the mirrored 4 paths, adds S_fwd and does WTA
 //    + parabola in registers; only int16 / float32 disparities leave the SM.
-//  * One warp owns one image row; lane l owns the contiguous disparities
-//    d = CPL*l .. CPL*l+CPL-1 as CPL/2 packed u16x2 registers.  A path update is
-//    DPX min-plus: VIMNMX.U16x2 / VIADDMNMX.U16x2, neighbours d+-1 by PRMT plus one
-//    SHFL each way, min over d by VIMNMX + CREDUX.MIN (__reduce_min_sync), and the
-//    normalisation "+C - m" is a single IADD3 with a two's-complement constant.
+//  * One warp owns one image row; the disparities are folded into pairs k = (k, Dp-1-k)
+//    and lane l holds pairs R*l .. R*l+R-1 (R = CPL/2) as packed u16x2 registers (see
+//    path_update).  A path update is DPX min-plus: VIADDMNMX.U16x2 / VIMNMX3.U16x2, the
+//    d+-1 neighbours are the sibling registers or one SHFL each way, min over d by
+//    VIMNMX + CREDUX.MIN (__reduce_min_sync), and the normalisation "+C - m" is a single
+//    IADD3 with a two's-complement constant.
 //  * The cost C is recomputed on the fly from the census windows (never stored); the
-//    window of census_match values slides one position per step by one SHFL.
-//  * Rows of a CTA run as a skewed wavefront: warp w processes position t - 2w at
-//    lockstep step t, so its three row-above predecessors (x-1, x, x+1) were produced
-//    at least one step earlier.  Row-above path vectors pass through a 4-slot shared
-//    memory ring per warp pair.  CTAs own bands of NW rows; the band's last row hands
-//    its vectors to the next band's CTA through global memory with a progress flag
-//    (release/acquire at gpu scope), prefetched by cp.async 8 positions ahead.  CTAs
-//    take tickets (atomicAdd) so a band only ever waits for an already-running band.
+//    two windows of census_match values (low / high halves) slide one position per
+//    step by one SHFL each.
+//  * Rows of a CTA run as a skewed wavefront: row w+1 consumes row w's path vectors
+//    through a shared-memory ring of position slots with full / empty mbarriers
+//    (synchronised in groups of positions).  CTAs own bands of up to NW rows (height
+//    chosen per call on the host); the band's last row hands its vectors to the next
+//    band's CTA through global memory with a progress flag published by a separate
+//    warp, prefetched by cp.async.  CTAs take tickets (atomicAdd) so a band only ever
+//    waits for an already-running band.
 #include <type_traits>
 
 #include "sgm_internal.cuh"
