@@ -34,8 +34,8 @@ struct sgm_handle {
     int16_t *lr_int = nullptr;      // [2*max_batch][H][W]
     float *lr_sub = nullptr;
     uint8_t *lr_valid = nullptr;
-    uint16_t *gbuf = nullptr;       // [4*max_batch][bands of the call][W][3][Dp] (<= nbands)
-    int *sync = nullptr;            // [1 + 4*max_batch*nbands]
+    uint16_t *gbuf = nullptr;       // 2 x [4*max_batch][bands of the call][W][3][Dp] (<= nbands)
+    int *sync = nullptr;            // sweep sync buffer (sgm::sweep_sync_ints ints)
     unsigned *eval_part = nullptr;  // [evaluate_max_blocks() + max_batch][12] + ticket
     // staging for the _host entry point (device): two slots so that back-to-back calls
     // pipeline (upload of call k+1 and download of call k-1 overlap the kernels of call k)
@@ -228,9 +228,11 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     if (e == cudaSuccess) e = dalloc(&h->lr_int, nv / 2 * npx);
     if (e == cudaSuccess) e = dalloc(&h->lr_sub, nv / 2 * npx);
     if (e == cudaSuccess) e = dalloc(&h->lr_valid, nv / 2 * npx);
-    if (e == cudaSuccess) e = dalloc(&h->gbuf, nv * size_t(h->nbands) * size_t(W) * 3 * size_t(h->dp));
-    if (e == cudaSuccess) e = dalloc(&h->sync, 1 + nv * size_t(h->nbands));
-    if (e == cudaSuccess) e = dalloc(&h->sync_host, 1 + nv * size_t(h->nbands));
+    // band handoff rows: one half per sweep (the two sweeps of a call overlap)
+    if (e == cudaSuccess) e = dalloc(&h->gbuf, 2 * nv * size_t(h->nbands) * size_t(W) * 3 * size_t(h->dp));
+    const size_t nsync = sgm::sweep_sync_ints(int(nv), h->nbands);
+    if (e == cudaSuccess) e = dalloc(&h->sync, nsync);
+    if (e == cudaSuccess) e = dalloc(&h->sync_host, nsync);
     const size_t eval_rows = size_t(sgm::evaluate_max_blocks()) + size_t(p->max_batch);
     if (e == cudaSuccess) e = dalloc(&h->eval_part, eval_rows * 12 + 1);
     if (e == cudaSuccess) e = cudaMemset(h->eval_part + eval_rows * 12, 0, sizeof(unsigned));
@@ -254,7 +256,7 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     for (cudaStream_t *sp : {&h->s_in, &h->s_comp, &h->s_out})
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking);
     for (int i = 0; i <= SGM_NUM_STAGES && e == cudaSuccess; ++i) e = cudaEventCreate(&h->ev[i]);
-    if (e == cudaSuccess) e = cudaMemset(h->sync, 0, sizeof(int) * (1 + nv * size_t(h->nbands)));
+    if (e == cudaSuccess) e = cudaMemset(h->sync, 0, sizeof(int) * nsync);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaGetLastError();

@@ -50,6 +50,8 @@ struct SweepParams {
     uint16_t *gbuf;           // [view][band][W][3][Dp]
     int *progress;            // [view][band]
     int *ticket;              // CTA ticket counter (zeroed before launch)
+    int *fwd_done;            // [view] forward-sweep rows finished (the backward sweep's band 0
+                              // starts a view once it reaches H: the two launches overlap)
     unsigned long long *trace; // debug: per (ticket, warp) {start ns, end ns, smid, 0} or null
     int debug_flags;           // debug (env SGM_DEBUG_FLAGS): 1 = no inter-warp/band waits
     int one;                   // always 1 (opaque to the compiler: keeps adds on the FMA pipe)
@@ -115,6 +117,7 @@ cudaError_t launch_census(const uint8_t *const *imgs, int nimg, long long pitch,
                           int cw, int ch, uint64_t *out, long long out_stride, cudaStream_t st);
 cudaError_t launch_cost(const uint64_t *ref, const uint64_t *match, int W, int H, int D, int s,
                         int cmax, uint8_t *cost, cudaStream_t st);
+size_t sweep_sync_ints(int nviews, int nbands);   // ints of a call's sweep sync buffer
 cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool debug_s,
                           cudaStream_t st, cudaEvent_t mid_ev_a, cudaEvent_t mid_ev_b,
                           int *launches);

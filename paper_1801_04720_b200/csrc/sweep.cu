@@ -102,6 +102,11 @@ __device__ __forceinline__ int ld_relaxed_gpu(const int *p) {
     asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_relaxed_gpu(int *p, int v) {
     asm volatile("st.relaxed.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
@@ -255,6 +260,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
+    // Programmatic dependent launch: the backward sweep's CTAs may be scheduled once every
+    // forward CTA has started (so they never hold an SM a forward CTA still needs); they
+    // then wait per view on fwd_done, not for the whole forward grid.
+    if (!BWD) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int ticket = s_ticket;
     const int band = ticket / p.nviews;
     const int view = ticket - band * p.nviews;
@@ -291,6 +300,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     if (warp >= hb) return;                         // rows past the band
     const bool has_row_below = (warp < hb - 1) && !(p.debug_flags & 1);
     const int y = BWD ? (H - 1 - j) : j;
+    if (BWD) {
+        // the view's forward sweep must be complete before this row reads S_fwd (the
+        // S_fwd prefetch below runs before any other synchronisation)
+        // every lane polls (one request per poll): a lane-0-only loop made the compiler
+        // treat the warp as possibly diverged and wrap every later SHFL / CREDUX in
+        // WARPSYNC (backward sweep 3.36 -> 4.85 ms)
+#pragma unroll 1
+        for (int spins = 0; spins < (1 << 26); ++spins) {
+            const bool done = ld_acquire_gpu(p.fwd_done + view) >= H;
+            if (__all_sync(0xffffffffu, done)) break;
+            __nanosleep(256);
+        }
+    }
 
     const uint64_t *ref, *match;
     int mirror;
@@ -683,6 +705,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
         mbar_arrive(my_full + (((W - 1) / G) % RG));
     }
     if (band_input) cp_async_wait<0>();
+    if (!BWD) {                                     // this row's S_fwd is complete
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(p.fwd_done + view, 1);
+        }
+    }
     if (trace && lane == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -690,23 +719,33 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     }
 }
 
+// The two sweeps of one call.  Sync buffer (zeroed once, before the forward launch):
+//   [ticket, progress[nviews*nbands]] forward, the same for the backward sweep, fwd_done[nviews]
+// and the band-handoff buffer is split in two, so that the backward sweep (launched with
+// programmatic stream serialisation) can overlap the forward sweep's last wave.
 template <int CPL, bool C64, int NW, bool PAD>
 cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cudaEvent_t ev_mid_a,
                         cudaEvent_t ev_mid_b, int *launches, int *sync_buf, size_t sync_bytes) {
     (void)debug_s;
     const dim3 grid(p.nviews * p.nbands), block((NW + 1) * 32);
+    const size_t per = 1 + size_t(p.nviews) * p.nbands;
+    SweepParams pf = p, pb = p;
+    pf.ticket = sync_buf; pf.progress = sync_buf + 1;
+    pb.ticket = sync_buf + per; pb.progress = sync_buf + per + 1;
+    pf.fwd_done = pb.fwd_done = sync_buf + 2 * per;
+    pb.gbuf = p.gbuf + size_t(p.nviews) * p.nbands * size_t(p.W) * 3 * p.Dp;
     cudaError_t e;
+    if ((e = cudaMemsetAsync(sync_buf, 0, sync_bytes, st)) != cudaSuccess) return e;
     {
         constexpr size_t sm = Sweep<CPL, C64, false, NW>::smem_bytes();
         auto k = sweep_kernel<CPL, C64, false, NW, PAD, false>;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))) != cudaSuccess) return e;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
-        if ((e = cudaMemsetAsync(sync_buf, 0, sync_bytes, st)) != cudaSuccess) return e;
-        k<<<grid, block, sm, st>>>(p);
+        k<<<grid, block, sm, st>>>(pf);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (launches) ++*launches;
     }
-    if (ev_mid_a) cudaEventRecord(ev_mid_a, st);
+    if (ev_mid_a) cudaEventRecord(ev_mid_a, st);    // (timing mode: no overlap)
     if (ev_mid_b) cudaEventRecord(ev_mid_b, st);
     {
         constexpr size_t sm = Sweep<CPL, C64, true, NW>::smem_bytes();   // same for PAD
@@ -715,9 +754,17 @@ cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cud
         auto k = p.sout ? sweep_kernel<CPL, C64, true, NW, true, true> : sweep_kernel<CPL, C64, true, NW, true, false>;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))) != cudaSuccess) return e;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
-        if ((e = cudaMemsetAsync(sync_buf, 0, sync_bytes, st)) != cudaSuccess) return e;
-        k<<<grid, block, sm, st>>>(p);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = block;
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if ((e = cudaLaunchKernelEx(&cfg, k, pb)) != cudaSuccess) return e;
         if (launches) ++*launches;
     }
     return cudaSuccess;
@@ -726,13 +773,14 @@ cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cud
 }  // namespace
 
 int sweep_warps_for(int cpl) { (void)cpl; return kBandRowsMax; }
+size_t sweep_sync_ints(int nviews, int nbands) { return 2 * (1 + size_t(nviews) * nbands) + size_t(nviews); }
 
 cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool debug_s,
                           cudaStream_t st, cudaEvent_t mid_ev_a, cudaEvent_t mid_ev_b,
                           int *launches) {
-    // ticket + progress live at p.ticket (ticket first, then progress[nviews*nbands])
+    // the call's sync buffer starts at p.ticket (layout: launch_pair)
     int *sync_buf = p.ticket;
-    const size_t sync_bytes = sizeof(int) * (1 + size_t(p.nviews) * p.nbands);
+    const size_t sync_bytes = sizeof(int) * sweep_sync_ints(p.nviews, p.nbands);
     if (nw != sweep_warps_for(cpl)) return cudaErrorInvalidValue;
 #define SGM_CASE(CPL_, C64_)                                                                   \
     if (cpl == CPL_ && c64 == C64_) {                                                          \
