@@ -57,6 +57,28 @@ __device__ __forceinline__ uint64_t census_px(const uint8_t *s, int bh, int gx, 
     return bits;
 }
 
+// interior tiles: every window sample inside the image, no clamping (the common case)
+template <int CW, int CH>
+__device__ __forceinline__ uint64_t census_px_in(const uint8_t *s, int lx, int ly) {
+    constexpr int rx = CW / 2, ry = CH / 2;
+    const uint8_t *ctr = s + (ly + ry) * kBoxW + (lx + kHaloX);
+    const int c = ctr[0];
+    uint32_t lo = 0, hi = 0;
+    int k = 0;
+#pragma unroll
+    for (int dy = -ry; dy <= ry; ++dy) {
+#pragma unroll
+        for (int dx = -rx; dx <= rx; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            const uint32_t bit = uint32_t(int(ctr[dy * kBoxW + dx]) < c);
+            if (k < 32) lo |= bit << k;
+            else hi |= bit << (k - 32);
+            ++k;
+        }
+    }
+    return uint64_t(lo) | (uint64_t(hi) << 32);
+}
+
 template <int CW, int CH>
 __global__ void __launch_bounds__(kThreads) census_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           CensusParams prm, uint64_t *out,
@@ -97,6 +119,14 @@ __global__ void __launch_bounds__(kThreads) census_kernel(const __grid_constant_
         }
     }
     uint64_t *o = out + (long long)img * out_stride;
+    if (CW > 0 && x0 - CW / 2 >= 0 && x0 + kTileW + CW / 2 <= prm.W && y0 - CH / 2 >= 0 &&
+        y0 + kTileH + CH / 2 <= prm.H) {
+        for (int k = threadIdx.x; k < kTileW * kTileH; k += kThreads) {
+            const int lx = k % kTileW, ly = k / kTileW;
+            o[(long long)(y0 + ly) * prm.W + x0 + lx] = census_px_in<(CW > 0 ? CW : 1), (CH > 0 ? CH : 1)>(tile, lx, ly);
+        }
+        return;
+    }
     for (int k = threadIdx.x; k < kTileW * kTileH; k += kThreads) {
         const int lx = k % kTileW, ly = k / kTileW;
         const int gx = x0 + lx, gy = y0 + ly;

@@ -59,11 +59,16 @@ nv = 4 * F
 bandstart = st[:, 0].reshape(-1, nv)   # [band][view]
 bl = np.diff(bandstart, axis=0)
 print(f"band-to-band start lag median {np.median(bl):.2f} us")
-# time when each SM was busy: union of CTA spans per SM
+# time when each SM was busy: union of CTA spans per SM (valid warps only)
+stv = np.where(valid, st, np.inf).min(axis=1)
+env = np.where(valid, en, -np.inf).max(axis=1)
+ok = np.isfinite(stv) & np.isfinite(env)
 busy = 0.0
 sms = t[:, 0, 2].astype(int)
-for smid in set(sms.tolist()):
-    iv = sorted(zip(st.min(axis=1)[sms == smid], en.max(axis=1)[sms == smid]))
+span = env[ok].max()
+for smid in set(sms[ok].tolist()):
+    sel = ok & (sms == smid)
+    iv = sorted(zip(stv[sel], env[sel]))
     cur_s, cur_e = iv[0]
     for a, b in iv[1:]:
         if a > cur_e:
@@ -72,4 +77,10 @@ for smid in set(sms.tolist()):
         else:
             cur_e = max(cur_e, b)
     busy += cur_e - cur_s
-print(f"SM busy fraction over the kernel span: {busy / (len(set(sms.tolist())) * en[valid].max()):.3f}")
+nsm = len(set(sms[ok].tolist()))
+print(f"SM busy fraction over the kernel span: {busy / (nsm * span):.3f}")
+# per band index: mean warp-loop duration (includes waiting for the band above)
+nb_ = ncta // (4 * F)
+dur_c = np.where(valid, dur, np.nan)
+mean_by_band = [np.nanmean(dur_c[b * 4 * F:(b + 1) * 4 * F]) for b in range(nb_)]
+print("mean warp loop us by band:", np.round(mean_by_band, 0))
