@@ -54,13 +54,14 @@ __global__ void wta_kernel(const uint16_t *__restrict__ agg, int W, int H, int D
 }
 
 // ------------------------------------------------------------------ LR check
+// grid (ceil(W / blockDim.x), H, pairs): no index division (a 64-bit division per pixel
+// made these small kernels instruction-bound)
 __global__ void lr_kernel(const LrParams p) {
-    const long long npx = (long long)p.W * p.H;
-    const long long total = npx * p.npairs;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long pair = idx / npx, px = idx - pair * npx;
-        const int x = int(px % p.W);
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= p.W) return;
+    const long long pair = blockIdx.z;
+    const int px = int(blockIdx.y) * p.W + x;      // W * H < 2^31 (sgm_create)
+    {
         const int16_t *dl = p.dl + pair * p.in_stride_l;
         const float *dls = p.dls + pair * p.in_stride_l;
         const int16_t *dr = p.dr + pair * p.in_stride_r;
@@ -82,12 +83,13 @@ __global__ void lr_kernel(const LrParams p) {
 // One thread per pixel, float4 stores.  Validity decisions are taken in float32 exactly
 // like the oracle's (x' = (float)x + u, floor, fractional part, taps with nonzero weight).
 __global__ void combine_kernel(const CombineParams p) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= p.W) return;
+    const int y = blockIdx.y;
+    const long long q = blockIdx.z;
     const long long npx = (long long)p.W * p.H;
-    const long long total = npx * p.nquads;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long q = idx / npx, px = idx - q * npx;
-        const int x = int(px % p.W), y = int(px / p.W);
+    const long long px = (long long)y * p.W + x, idx = q * npx + px;
+    {
         const float2 uv = reinterpret_cast<const float2 *>(p.flow)[idx];
         const float *d0 = p.d0 + q * p.disp_stride;
         const float *d1 = p.d1 + q * p.disp_stride;
@@ -188,14 +190,14 @@ cudaError_t launch_repitch(const uint8_t *src, uint8_t *dst, int W, long long pi
 }
 
 cudaError_t launch_lr(const LrParams &p, cudaStream_t st) {
-    const long long n = (long long)p.W * p.H * p.npairs;
-    lr_kernel<<<grid_for(n, 256), 256, 0, st>>>(p);
+    if (p.npairs < 1 || p.npairs > 65535 || p.H > 65535) return cudaErrorInvalidValue;
+    lr_kernel<<<dim3((p.W + 127) / 128, p.H, p.npairs), 128, 0, st>>>(p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_combine(const CombineParams &p, cudaStream_t st) {
-    const long long n = (long long)p.W * p.H * p.nquads;
-    combine_kernel<<<grid_for(n, 256), 256, 0, st>>>(p);
+    if (p.nquads < 1 || p.nquads > 65535 || p.H > 65535) return cudaErrorInvalidValue;
+    combine_kernel<<<dim3((p.W + 127) / 128, p.H, p.nquads), 128, 0, st>>>(p);
     return cudaGetLastError();
 }
 
