@@ -716,17 +716,17 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
                 // warps that have work
                 while (hand_tag(e = ring_in[i & (kRowRing - 1)]) != i + 1) __nanosleep(20);
             } else {
-                // band handoff through L2: wait until the whole 32-position chunk is
-                // published, one round trip per poll, then read it from registers
-                if ((i & 31) == 0) {
-                    while (true) {
-                        hbuf = i + lane < W ? ld_relaxed_u64(hin + i + lane) : 0ull;
-                        const bool ready = i + lane >= W || hand_tag(hbuf) == i + lane + 1;
-                        if (__all_sync(0xffffffffu, ready)) break;
-                        __nanosleep(128);
-                    }
-                }
+                // band handoff through L2: the 32 positions of a chunk are fetched in one
+                // round trip (lane l holds position 32c + l); a position not yet published
+                // re-fetches the chunk, so the band runs one position behind its producer
+                if ((i & 31) == 0) hbuf = i + lane < W ? ld_relaxed_u64(hin + i + lane) : 0ull;
                 e = __shfl_sync(0xffffffffu, hbuf, i & 31);
+                while (hand_tag(e) != i + 1) {
+                    __nanosleep(64);
+                    const int q = (i & ~31) + lane;
+                    hbuf = q < W ? ld_relaxed_u64(hin + q) : 0ull;
+                    e = __shfl_sync(0xffffffffu, hbuf, i & 31);
+                }
             }
             vv = hand_vec(e);
         }
