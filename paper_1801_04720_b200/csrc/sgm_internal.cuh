@@ -8,20 +8,16 @@
 namespace sgm {
 
 // ----------------------------------------------------------------- constants
-constexpr int kWarp = 32;
 constexpr int kRing = 8;        // row->row handoff ring (positions) for CPL > 4
 constexpr int kRingWide = 16;   // ... for CPL <= 4 (fits 16 warps x 16 x 3 x 256 B)
 constexpr int kRing0 = 16;      // band-input ring of warp 0 (positions)
-constexpr int kLook = 8;        // band-input prefetch distance (positions)
-constexpr int kPublish = 8;     // band-output progress publication granularity (positions)
+constexpr int kPublish = 8;     // forward sweep's band-output publication granularity (positions)
 constexpr int kPubDepth = 4;    // producer -> publisher-warp handoff depth (groups)
 // SGM sweep bands: a CTA carries one band of up to kBandRowsMax rows (one compute warp per
 // row); the host picks the band height per call in [kBandRowsMin, kBandRowsMax] so that
 // the CTA count fills whole waves of the SMs (band_geometry in api.cu)
 constexpr int kBandRowsMax = 17;
 constexpr int kBandRowsMin = 10;
-constexpr uint32_t kSent = 0x7FFF7FFFu;   // "no neighbour" path cost (both halves)
-constexpr uint32_t kPadCost = 0x10001000u; // OR-ed into padded disparities d >= D
 
 // ----------------------------------------------------------------- kernel params
 struct SweepParams {
