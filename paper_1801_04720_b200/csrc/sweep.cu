@@ -175,7 +175,9 @@ struct Sweep {
     // group g needs the producer to have finished position (g+1)G, and the producer may
     // run at most ~RS-G positions ahead; RS = 16 needs 16 x 3 x Dp x 2 bytes per warp.
     static constexpr int RS = (CPL <= 4) ? kRingWide : kRing;
-    static constexpr int G = (CPL <= 4) ? CPL : 1;   // groups align with the unrolled block
+    // groups align with the unrolled block; CPL > 4 (8 ring slots): 2-position groups
+    // (lead window [3, 6]) instead of per-position sync: Wide 15.6 -> 11.5 ms
+    static constexpr int G = (CPL <= 4) ? CPL : 2;
     static constexpr int RG = RS / G;              // groups per ring
     // band-input ring of warp 0 (positions) and census prefetch entries per warp: trimmed
     // for 8 cells per lane so that 16-row bands fit the 227 KB of shared memory
