@@ -349,9 +349,11 @@ __device__ __forceinline__ unsigned half2_bits(int lo, int hi) {
 }
 
 // Packed database entry (64 B + norms): limbs of the 16 coefficients as half2 words,
-// word w = dims (2w, 2w+1); computed once per image by ff_knn_prep_kernel.
+// word w = dims (2w, 2w+1), stored in the order w = 0, 4, 1, 5, 2, 6, 3, 7 so that the two
+// words a fragment lane t needs (w = t and t + 4) are one 64-bit load; computed once per
+// image by ff_knn_prep_kernel.
 struct KnnEntry {
-    unsigned bh[8], bl[8];
+    uint2 bh[4], bl[4];           // bh[t] = {word t, word t + 4}
 };
 
 // norms are stored per problem with a stride n_pad = n rounded up to 4 (16-byte aligned
@@ -365,10 +367,12 @@ __global__ void ff_knn_prep_kernel(const int32_t *__restrict__ desc, int n, int 
         const int32_t *c = desc + e * 16;
         KnnEntry k;
         long long bn = 0;
+        unsigned *kh = reinterpret_cast<unsigned *>(k.bh), *kl = reinterpret_cast<unsigned *>(k.bl);
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
-            k.bh[w] = half2_bits(c[2 * w] >> 7, c[2 * w + 1] >> 7);
-            k.bl[w] = half2_bits(c[2 * w] & 127, c[2 * w + 1] & 127);
+            const int slot = 2 * (w & 3) + (w >> 2);
+            kh[slot] = half2_bits(c[2 * w] >> 7, c[2 * w + 1] >> 7);
+            kl[slot] = half2_bits(c[2 * w] & 127, c[2 * w + 1] & 127);
             bn += (long long)c[2 * w] * c[2 * w] + (long long)c[2 * w + 1] * c[2 * w + 1];
         }
         ent[e] = k;
@@ -402,8 +406,8 @@ __global__ void __launch_bounds__(kKnnWarps * 32) ff_knn_mma_kernel(const KnnEnt
     // A fragments (m16n8k16, row-major 16 x 16): a0 = row g, k 2t..2t+1; a1 = row g+8;
     // a2 = row g, k 2t+8..2t+9; a3 = row g+8, k 2t+8..2t+9
     unsigned ah[4] = {0u, 0u, 0u, 0u}, al[4] = {0u, 0u, 0u, 0u};
-    if (r0 < n) { ah[0] = eq[r0].bh[t]; ah[2] = eq[r0].bh[t + 4]; al[0] = eq[r0].bl[t]; al[2] = eq[r0].bl[t + 4]; }
-    if (r1 < n) { ah[1] = eq[r1].bh[t]; ah[3] = eq[r1].bh[t + 4]; al[1] = eq[r1].bl[t]; al[3] = eq[r1].bl[t + 4]; }
+    if (r0 < n) { ah[0] = eq[r0].bh[t].x; ah[2] = eq[r0].bh[t].y; al[0] = eq[r0].bl[t].x; al[2] = eq[r0].bl[t].y; }
+    if (r1 < n) { ah[1] = eq[r1].bh[t].x; ah[3] = eq[r1].bh[t].y; al[1] = eq[r1].bl[t].x; al[3] = eq[r1].bl[t].y; }
     const long long qn0 = r0 < n ? nq[r0] : 0, qn1 = r1 < n ? nq[r1] : 0;
     KList L0, L1;
     klist_init(L0);
@@ -466,7 +470,8 @@ __global__ void __launch_bounds__(kKnnWarps * 32) ff_knn_mma_kernel(const KnnEnt
         for (int cg = 0; cg < kMmaTile / 8; ++cg) {
             // B fragment (16 x 8, col): b0 = k 2t..2t+1, b1 = k 2t+8..2t+9 of column g
             const KnnEntry &E = sE[b][cg * 8 + g];
-            const unsigned bh0 = E.bh[t], bh1 = E.bh[t + 4], bl0 = E.bl[t], bl1 = E.bl[t + 4];
+            const uint2 bhv = E.bh[t], blv = E.bl[t];
+            const unsigned bh0 = bhv.x, bh1 = bhv.y, bl0 = blv.x, bl1 = blv.y;
             float c1[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f}, c3[4] = {0.f, 0.f, 0.f, 0.f};
             mma_f16(c1, ah, bh0, bh1);              // sum qh bh
             mma_f16(c2, ah, bl0, bl1);              // + sum qh bl
