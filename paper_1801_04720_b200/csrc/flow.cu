@@ -467,6 +467,9 @@ __global__ void __launch_bounds__(kKnnWarps * 32) ff_knn_mma_kernel(const KnnEnt
             if (o1 < thr1 || (o1 == thr1 && oi1 < thr1_i)) { thr1 = o1; thr1_i = oi1; }
         }
         float lim0 = float(thr0) + kMargin, lim1 = float(thr1) + kMargin;
+        // screen in the form dot >= (bn + qn - lim) / 2: per element two FFMA for the dot, one
+        // FADD and one FSETP (the row part is updated with the bound)
+        float rt0 = 0.5f * (qn0f - lim0), rt1 = 0.5f * (qn1f - lim1);
         for (int cg = 0; cg < kMmaTile / 8; ++cg) {
             // B fragment (16 x 8, col): b0 = k 2t..2t+1, b1 = k 2t+8..2t+9 of column g
             const KnnEntry &E = sE[b][cg * 8 + g];
@@ -479,36 +482,39 @@ __global__ void __launch_bounds__(kKnnWarps * 32) ff_knn_mma_kernel(const KnnEnt
             mma_f16(c3, al, bl0, bl1);              // sum ql bl
             // fp32 screen of the 4 elements first; the exact path runs only when some lane
             // of the warp has a survivor (rare once the lists have filled)
-            float df[4];
-            unsigned pass = 0u;
+            float dotf[4];
+            bool pass = false;
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) {
-                const float bnf = sNf[b][cg * 8 + 2 * t + jj];
+                const float bnh = 0.5f * sNf[b][cg * 8 + 2 * t + jj];
 #pragma unroll
                 for (int rr = 0; rr < 2; ++rr) {
-                    const float dotf = fmaf(16384.f, c1[2 * rr + jj], fmaf(128.f, c2[2 * rr + jj], c3[2 * rr + jj]));
-                    df[2 * rr + jj] = fmaf(-2.f, dotf, (rr ? qn1f : qn0f) + bnf);
-                    pass |= (df[2 * rr + jj] <= (rr ? lim1 : lim0) ? 1u : 0u) << (2 * rr + jj);
+                    dotf[2 * rr + jj] = fmaf(16384.f, c1[2 * rr + jj], fmaf(128.f, c2[2 * rr + jj], c3[2 * rr + jj]));
+                    pass |= dotf[2 * rr + jj] >= bnh + (rr ? rt1 : rt0);
                 }
             }
-            if (!__any_sync(0xffffffffu, pass != 0u)) continue;
+            if (!__any_sync(0xffffffffu, pass)) continue;
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) {
                 const int col = cg * 8 + 2 * t + jj;
                 const int idx = base + col;
+                const float bnf = sNf[b][col];
 #pragma unroll
                 for (int rr = 0; rr < 2; ++rr) {
                     // re-test against the bound as updated by earlier insertions
-                    if (df[2 * rr + jj] <= (rr ? lim1 : lim0) && idx < n) {
+                    const float df = fmaf(-2.f, dotf[2 * rr + jj], (rr ? qn1f : qn0f) + bnf);
+                    if (df <= (rr ? lim1 : lim0) && idx < n) {
                         const long long dot = 16384ll * (long long)c1[2 * rr + jj] +
                                               128ll * (long long)c2[2 * rr + jj] + (long long)c3[2 * rr + jj];
                         const long long d = (rr ? qn1 : qn0) + sN[b][col] - 2 * dot;
                         if (rr) {
                             KOFFER(L1, thr1, thr1_i, d, idx);
                             lim1 = float(thr1) + kMargin;
+                            rt1 = 0.5f * (qn1f - lim1);
                         } else {
                             KOFFER(L0, thr0, thr0_i, d, idx);
                             lim0 = float(thr0) + kMargin;
+                            rt0 = 0.5f * (qn0f - lim0);
                         }
                     }
                 }
