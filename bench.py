@@ -55,17 +55,20 @@ def parse():
 
 # ---------------------------------------------------------------------------- helpers
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.  nvidia-smi is
+    started (and waited for: its first sample can take a few hundred ms) before the timed
+    region; only samples stamped between begin() and stop() are kept."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []                      # (monotonic time, fields)
         self.proc = None
+        self.t_begin = None
 
-    def start(self):
+    def start(self, wait_s=10.0):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -75,23 +78,35 @@ class ClockSampler:
             self.t.start()
         except OSError:
             self.proc = None
+            return
+        t0 = time.monotonic()
+        while not self.rows and time.monotonic() - t0 < wait_s and self.proc.poll() is None:
+            time.sleep(0.01)
+
+    def begin(self):
+        self.t_begin = time.monotonic()
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.monotonic(), [c.strip() for c in line.split(",")]))
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t_end = time.monotonic()
+        time.sleep(0.03)                    # the sample in flight at the end of the region
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
+        t_begin = self.t_begin if self.t_begin is not None else 0.0
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        for t, r in self.rows:
+            if t < t_begin or t > t_end + 0.025:
+                continue
             try:
                 sm.append(float(r[1]))
                 smax.append(float(r[2]))
@@ -265,10 +280,11 @@ def main():
     launches_per_step = 5
     stage_ms = {}
     clocks = ClockSampler(local)
+    clocks.start()                          # before the barrier: nvidia-smi needs a moment
     if pg is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clocks.start()
+    clocks.begin()
     total_ms = 0.0
     with torch.cuda.stream(stream):
         for _ in range(args.steps):
