@@ -180,7 +180,7 @@ struct Sweep {
     static constexpr int G = (CPL <= 4) ? CPL : 2;
     static constexpr int RG = RS / G;              // groups per ring
     // band-input ring of warp 0 (positions) and census prefetch entries per warp: trimmed
-    // for 8 cells per lane so that 16-row bands fit the 227 KB of shared memory
+    // for 8 cells per lane so that 17-row bands fit the 227 KB of shared memory
     static constexpr int RING0 = (CPL <= 6) ? kRing0 : kRing0 / 2;
     static constexpr int CEN = BWD ? 0 : 64;       // the backward sweep reads no census
 
