@@ -19,10 +19,19 @@
  *    synchronisation (except sgm_create / sgm_destroy).  Asynchronous device
  *    faults surface at the caller's next synchronisation.
  *  - Argument errors are detected synchronously, before anything is enqueued,
- *    and return SGM_ERR_INVALID_ARGUMENT.  Launch failures return
+ *    and return SGM_ERR_INVALID_ARGUMENT.  Every CUDA failure seen after
+ *    validation (launch or copy errors, whatever their CUDA code) returns
  *    SGM_ERR_CUDA.  No C++ exception crosses this ABI.
- *  - A handle is bound to one device and is not re-entrant: use one handle per
- *    concurrent stream.  Identical inputs give bit-identical outputs.
+ *  - Device faults: the sweeps' cross-CTA waits are bounded; a wait that times
+ *    out (a scheduling / logic error) writes a fault code into a host-mapped
+ *    word of the handle, the affected rows store no disparities, and every
+ *    later compute entry point of the handle returns SGM_ERR_CUDA until
+ *    sgm_get_device_error(h, &code, 1) clears the fault.
+ *  - A handle is bound to one device: every entry point makes that device
+ *    current for the duration of the call and restores the caller's current
+ *    device (of this library's runtime) on return.  A handle is not
+ *    re-entrant: use one handle per concurrent stream.  Identical inputs give
+ *    bit-identical outputs.
  */
 #ifndef SGMSF_H
 #define SGMSF_H
@@ -90,12 +99,15 @@ typedef struct sgm_sceneflow_out {
     uint8_t *disp_valid;    /* [n][2][H][W] LR masks of D0, D1 */
 } sgm_sceneflow_out;
 
-/* Create a handle on `device` (cudaSetDevice is called): validates `p`
- * (SGM_ERR_INVALID_ARGUMENT on: W or H < 1, D outside 1..256, even census
- * side, a 1x1 census window (no bits), census_w*census_h-1 > 63, P1 < 0, P2 < P1, C_max+P2 > 255, T < 0,
- * bilinear_rule not 0/1, max_batch < 1) and allocates all scratch for
- * max_batch quads (SGM_ERR_OUT_OF_MEMORY if that fails).  Synchronous.
- * `*out` is set only on SGM_OK. */
+/* Create a handle on `device`: validates `p` (SGM_ERR_INVALID_ARGUMENT on: W
+ * or H < 1, D outside 1..256, even census side, a 1x1 census window (no bits),
+ * census_w*census_h-1 > 63, P1 < 0, P2 < P1, C_max+P2 > 255, T < 0,
+ * bilinear_rule not 0/1, max_batch < 1; SGM_ERR_UNSUPPORTED on H > 65535,
+ * W*H >= 2^31, 2*max_batch > 65535 or a census side > 17 -- launch-geometry
+ * limits of the kernels, checked here so that no later call fails half-way
+ * through its launches) and allocates all scratch for max_batch quads
+ * (SGM_ERR_OUT_OF_MEMORY if that fails).  Synchronous; the caller's current
+ * device is restored.  `*out` is set only on SGM_OK. */
 SGM_API sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out);
 
 /* Free the handle and its scratch after synchronising the device.  NULL-safe. */
@@ -283,6 +295,19 @@ SGM_API sgm_status sgm_get_geometry(sgm_handle *h, int32_t *dp, int32_t *cells_p
  * SM id, 0} of its row loop at index (ticket * (sweep_warps + 1) + warp) * 4 (the last
  * launch wins).  NULL disables it (default). */
 SGM_API sgm_status sgm_debug_set_trace(sgm_handle *h, uint64_t *trace);
+
+/* Device fault word of the handle (see "Device faults" above): *code = 0 (no fault),
+ * 1 (a backward-sweep row timed out waiting for its view's forward sweep) or 2 (a band
+ * timed out waiting for the band above it).  Reads host memory: call it after
+ * synchronising the stream of the call in question.  clear != 0 resets the word, after
+ * which the entry points work again.  code may be NULL. */
+SGM_API sgm_status sgm_get_device_error(sgm_handle *h, int32_t *code, int32_t clear);
+
+/* Debugging / fault-injection flags of the sweeps (default: env SGM_DEBUG_FLAGS or 0):
+ * 1 = no inter-warp / inter-band waits, 2 = no band handoff (both give WRONG results;
+ * timing experiments only), 4 = force every bounded cross-CTA wait to time out (tests
+ * the fault reporting).  SGM_ERR_INVALID_ARGUMENT outside 0..7. */
+SGM_API sgm_status sgm_debug_set_flags(sgm_handle *h, int32_t flags);
 
 #ifdef __cplusplus
 }

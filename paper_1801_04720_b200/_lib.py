@@ -26,6 +26,7 @@ EXPORTS = (
     "sgm_scene_flow_host", "sgm_set_timing", "sgm_read_timing", "sgm_stage_name",
     "sgm_launch_count", "sgm_get_geometry", "sgm_last_error_string", "sgm_debug_set_trace",
     "sgm_evaluate", "sgm_scene_flow_stream", "sgm_scene_flow_stream_host",
+    "sgm_get_device_error", "sgm_debug_set_flags",
     # include/sgmflow.h
     "sgm_flow_create", "sgm_flow_destroy", "sgm_flow_last_error_string", "sgm_flow_launch_count",
     "sgm_flow", "sgm_flow_field", "sgm_flow_descriptors", "sgm_flow_patch_cost",
@@ -130,6 +131,8 @@ def load(path: str | None = None):
         "sgm_stage_name": (ctypes.c_char_p, [I32]),
         "sgm_launch_count": (I64, [P]),
         "sgm_debug_set_trace": (st, [P, P]),
+        "sgm_get_device_error": (st, [P, ctypes.POINTER(I32), I32]),
+        "sgm_debug_set_flags": (st, [P, I32]),
         "sgm_get_geometry": (st, [P, ctypes.POINTER(I32), ctypes.POINTER(I32),
                                   ctypes.POINTER(I32), ctypes.POINTER(I32)]),
         "sgm_flow_create": (st, [ctypes.POINTER(SgmFlowParams), I32, ctypes.POINTER(P)]),

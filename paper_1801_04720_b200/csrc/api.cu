@@ -60,6 +60,11 @@ struct sgm_handle {
     cudaEvent_t ev[SGM_NUM_STAGES + 1] = {};
     long long launches = 0;
     unsigned long long *trace = nullptr;   // debug timeline buffer (caller-owned, device)
+    int debug_flags = 0;                   // SweepParams::debug_flags (env SGM_DEBUG_FLAGS)
+    // device fault word: mapped pinned host memory the sweeps write a fault code into when a
+    // bounded cross-CTA wait times out; every compute entry point checks it (no sync needed)
+    int *err_host = nullptr;
+    int *err_dev = nullptr;
 };
 
 namespace {
@@ -69,10 +74,30 @@ thread_local char g_last_error[256] = "no error";
 sgm_status from_cuda(cudaError_t e) {
     if (e == cudaSuccess) return SGM_OK;
     snprintf(g_last_error, sizeof(g_last_error), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    // argument errors are caught by the entry points' validation before anything is
+    // enqueued; a CUDA error seen afterwards (any code) is a CUDA failure
     if (e == cudaErrorMemoryAllocation) return SGM_ERR_OUT_OF_MEMORY;
-    if (e == cudaErrorInvalidValue) return SGM_ERR_INVALID_ARGUMENT;
     return SGM_ERR_CUDA;
 }
+
+// A fault word set by an earlier kernel (sticky until sgm_get_device_error clears it)
+// makes every compute entry point fail; the word is host memory, so no sync is needed.
+bool device_faulted(const sgm_handle *h) {
+    const int code = h->err_host ? *reinterpret_cast<volatile const int *>(h->err_host) : 0;
+    if (code == 0) return false;
+    snprintf(g_last_error, sizeof(g_last_error),
+             "device fault %d: a sweep's cross-CTA wait timed out (%s); results of that call are "
+             "invalid -- sgm_get_device_error clears the fault", code,
+             code == sgm::kFaultFwdDone ? "forward sweep never completed" : "band input never published");
+    return true;
+}
+
+// Entry-point prologue: the handle's device becomes current for the call (restored on
+// return) and a pending device fault is reported.
+#define SGM_ENTRY(h)                                                  \
+    sgm::DeviceGuard guard_((h)->device);                             \
+    if (guard_.status != cudaSuccess) return from_cuda(guard_.status); \
+    if (device_faulted(h)) return SGM_ERR_CUDA;
 
 template <class T>
 cudaError_t dalloc(T **p, size_t count) {
@@ -84,6 +109,7 @@ void free_all(sgm_handle *h) {
                     h->gbuf, h->sync, h->sync_host, h->eval_part};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    if (h->err_host) cudaFreeHost(h->err_host);
     for (auto &st : h->stage) {
         void *sp[] = {st.img_dense, st.img, st.flow, st.fvalid, st.sf, st.p0, st.dp, st.vsf, st.v3,
                       st.di, st.ds, st.dv};
@@ -153,12 +179,9 @@ sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int *sync = nullp
     if (!sync) sync = h->sync;
     p.progress = sync + 1; p.ticket = sync;
     p.trace = h->trace;
-    static const int dbg = [] {
-        const char *e = getenv("SGM_DEBUG_FLAGS");
-        return e ? atoi(e) : 0;
-    }();
-    p.debug_flags = dbg;
+    p.debug_flags = h->debug_flags;
     p.one = 1;
+    p.err = h->err_dev;
     return p;
 }
 
@@ -199,6 +222,10 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     if (p->lr_threshold < 0 || (p->bilinear_rule != 0 && p->bilinear_rule != 1) || p->max_batch < 1)
         return SGM_ERR_INVALID_ARGUMENT;
     if ((long long)W * H * 4LL * p->max_batch > (1LL << 40)) return SGM_ERR_INVALID_ARGUMENT;
+    // launch-geometry limits of the per-pixel kernels (grid y = H, grid z = pairs / quads):
+    // checked here so that no later call can fail half-way through its launch sequence
+    if (H > 65535 || (long long)W * H >= (1LL << 31)) return SGM_ERR_UNSUPPORTED;
+    if (2LL * p->max_batch > 65535) return SGM_ERR_UNSUPPORTED;
 
     sgm_handle *h = new (std::nothrow) sgm_handle();
     if (!h) return SGM_ERR_OUT_OF_MEMORY;
@@ -212,8 +239,10 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     h->nbands = (H + sgm::kBandRowsMin - 1) / sgm::kBandRowsMin;
     h->npx = (long long)W * H;
     h->max_views = 4 * p->max_batch;
+    if (const char *dbg = getenv("SGM_DEBUG_FLAGS")) h->debug_flags = atoi(dbg);
 
-    cudaError_t e = cudaSetDevice(device);
+    sgm::DeviceGuard guard(device);
+    cudaError_t e = guard.status;
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, device);
     const size_t nv = size_t(h->max_views), npx = size_t(h->npx);
     h->stage_pitch = ((long long)W + 15) / 16 * 16;
@@ -257,6 +286,12 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking);
     for (int i = 0; i <= SGM_NUM_STAGES && e == cudaSuccess; ++i) e = cudaEventCreate(&h->ev[i]);
     if (e == cudaSuccess) e = cudaMemset(h->sync, 0, sizeof(int) * nsync);
+    if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void **>(&h->err_host), 4 * sizeof(int),
+                                            cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+        memset(h->err_host, 0, 4 * sizeof(int));
+        e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&h->err_dev), h->err_host, 0);
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -270,7 +305,7 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
 
 void sgm_destroy(sgm_handle *h) {
     if (!h) return;
-    cudaSetDevice(h->device);
+    sgm::DeviceGuard guard(h->device);
     cudaDeviceSynchronize();
     free_all(h);
     delete h;
@@ -298,6 +333,20 @@ sgm_status sgm_debug_set_trace(sgm_handle *h, uint64_t *trace) {
     return SGM_OK;
 }
 
+sgm_status sgm_debug_set_flags(sgm_handle *h, int32_t flags) {
+    if (!h || flags < 0 || flags > 7) return SGM_ERR_INVALID_ARGUMENT;
+    h->debug_flags = flags;
+    return SGM_OK;
+}
+
+sgm_status sgm_get_device_error(sgm_handle *h, int32_t *code, int32_t clear) {
+    if (!h) return SGM_ERR_INVALID_ARGUMENT;
+    volatile int *w = reinterpret_cast<volatile int *>(h->err_host);
+    if (code) *code = w ? *w : 0;
+    if (clear && w) *w = 0;
+    return SGM_OK;
+}
+
 sgm_status sgm_set_timing(sgm_handle *h, int32_t enable) {
     if (!h) return SGM_ERR_INVALID_ARGUMENT;
     h->timing = enable != 0;
@@ -307,6 +356,7 @@ sgm_status sgm_set_timing(sgm_handle *h, int32_t enable) {
 
 int32_t sgm_read_timing(sgm_handle *h, float *ms) {
     if (!h || !ms || !h->timed) return 0;
+    sgm::DeviceGuard guard(h->device);
     for (int i = 0; i < SGM_NUM_STAGES; ++i) {
         float t = 0.f;
         if (cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]) != cudaSuccess) {
@@ -323,6 +373,7 @@ sgm_status sgm_census(sgm_handle *h, const uint8_t *img, int64_t pitch_bytes, ui
     if (!h || !img || !census || pitch_bytes < h->prm.width || (pitch_bytes % 16) != 0 ||
         !aligned16(img))
         return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = sgm::launch_census_stack(img, (long long)h->prm.height * pitch_bytes, 1,
                                              pitch_bytes, h->prm.width, h->prm.height,
@@ -335,6 +386,7 @@ sgm_status sgm_cost(sgm_handle *h, const uint64_t *cen_left, const uint64_t *cen
                     int32_t view, uint8_t *cost, void *stream) {
     if (!h || !cen_left || !cen_right || !cost || (view != 0 && view != 1))
         return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     const uint64_t *ref = view == 0 ? cen_left : cen_right;
     const uint64_t *match = view == 0 ? cen_right : cen_left;
     cudaError_t e = sgm::launch_cost(ref, match, h->prm.width, h->prm.height, h->prm.num_disp,
@@ -348,6 +400,7 @@ sgm_status sgm_aggregate(sgm_handle *h, const uint64_t *cen_left, const uint64_t
                          int32_t view, uint16_t *agg, void *stream) {
     if (!h || !cen_left || !cen_right || !agg || (view != 0 && view != 1))
         return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     sgm::SweepParams p = sweep_params(h, 1);
     p.explicit_mode = 1;
     p.ref0 = view == 0 ? cen_left : cen_right;
@@ -365,6 +418,7 @@ sgm_status sgm_aggregate(sgm_handle *h, const uint64_t *cen_left, const uint64_t
 
 sgm_status sgm_wta(sgm_handle *h, const uint16_t *agg, int16_t *d_int, float *d_sub, void *stream) {
     if (!h || !agg || !d_int || !d_sub) return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     cudaError_t e = sgm::launch_wta(agg, h->prm.width, h->prm.height, h->prm.num_disp, d_int, d_sub,
                                     static_cast<cudaStream_t>(stream));
     if (e == cudaSuccess) ++h->launches;
@@ -376,6 +430,7 @@ sgm_status sgm_lr_check(sgm_handle *h, const int16_t *dl_int, const float *dl_su
                         void *stream) {
     if (!h || !dl_int || !dl_sub || !dr_int || !out_int || !out_sub || !valid)
         return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     sgm::LrParams p{};
     p.W = h->prm.width; p.H = h->prm.height; p.T = h->prm.lr_threshold;
     p.invalid = h->prm.invalid_disp; p.npairs = 1;
@@ -394,6 +449,7 @@ sgm_status sgm_disparity(sgm_handle *h, const uint8_t *left, const uint8_t *righ
     if (pitch_bytes < h->prm.width || (pitch_bytes % 16) != 0 || !aligned16(left) ||
         !aligned16(right))
         return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int W = h->prm.width, H = h->prm.height;
     cudaError_t e = sgm::launch_census_stack(left, (long long)H * pitch_bytes, 1, pitch_bytes, W, H,
@@ -432,6 +488,7 @@ sgm_status sgm_combine_sceneflow(sgm_handle *h, const float *d0, const uint8_t *
     if (!aligned16(sf) || (p0 && !aligned16(p0)) || (dp && !aligned16(dp)) ||
         (reinterpret_cast<uintptr_t>(flow) & 7))
         return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     sgm::CombineParams p{};
     p.W = h->prm.width; p.H = h->prm.height; p.rule = h->prm.bilinear_rule; p.nquads = 1;
     p.d0 = d0; p.d1 = d1; p.v0 = v0; p.v1 = v1; p.disp_stride = 0;
@@ -458,6 +515,7 @@ sgm_status sgm_evaluate(sgm_handle *h, int32_t n, const float *sf, const uint8_t
         (reinterpret_cast<uintptr_t>(gt_d0) & 3) || (reinterpret_cast<uintptr_t>(gt_d1) & 3) ||
         (reinterpret_cast<uintptr_t>(counts) & 7))
         return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     sgm::EvalParams p{};
     p.W = h->prm.width; p.H = h->prm.height; p.nquads = n;
     p.sf = sf; p.valid_sf = valid_sf; p.gt_d0 = gt_d0; p.gt_d1 = gt_d1; p.gt_flow = gt_flow;
@@ -468,6 +526,13 @@ sgm_status sgm_evaluate(sgm_handle *h, int32_t n, const float *sf, const uint8_t
     cudaError_t e = sgm::launch_evaluate(p, static_cast<cudaStream_t>(stream));
     if (e == cudaSuccess) ++h->launches;
     return from_cuda(e);
+}
+
+// 3D outputs need dp, valid_3d and a camera with f > 0, B > 0 (validated before any enqueue)
+static bool camera_ok(const sgm_sceneflow_out *out, const sgm_camera *cam) {
+    const bool want3d = out->p0 || out->dp || out->valid_3d;
+    if (!want3d) return true;
+    return out->dp && out->valid_3d && cam && cam->f_px > 0.f && cam->baseline_m > 0.f;
 }
 
 // The batched hot path.  Quad mode: images [n][4][H][pitch] = n independent quads, 2n
@@ -552,6 +617,8 @@ static sgm_status scene_flow_dev(sgm_handle *h, int32_t n, bool stream, const ui
         !aligned16(out->sf) || (out->p0 && !aligned16(out->p0)) || (out->dp && !aligned16(out->dp)) ||
         (reinterpret_cast<uintptr_t>(flow) & 7))
         return SGM_ERR_INVALID_ARGUMENT;
+    if (!camera_ok(out, cam)) return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     return scene_flow_impl(h, n, stream, images, pitch_bytes, flow, flow_valid, cam, out,
                            static_cast<cudaStream_t>(stream_));
 }
@@ -577,7 +644,8 @@ static sgm_status scene_flow_host_impl(sgm_handle *h, int32_t n, bool stream_mod
     const long long nimg = stream_mode ? 2LL * (n + 1) : 4LL * n;   // images in the batch
     const long long nmaps = nimg / 2;                                // LR-checked maps
     const bool want3d = out->p0 || out->dp || out->valid_3d;
-    if (want3d && (!out->dp || !out->valid_3d || !cam)) return SGM_ERR_INVALID_ARGUMENT;
+    if (!camera_ok(out, cam)) return SGM_ERR_INVALID_ARGUMENT;
+    SGM_ENTRY(h);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int W = h->prm.width, H = h->prm.height;
     const long long npx = h->npx;

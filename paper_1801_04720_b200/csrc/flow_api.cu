@@ -39,9 +39,13 @@ sgm_status ff_status(cudaError_t e) {
     if (e == cudaSuccess) return SGM_OK;
     snprintf(g_ff_error, sizeof(g_ff_error), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
     if (e == cudaErrorMemoryAllocation) return SGM_ERR_OUT_OF_MEMORY;
-    if (e == cudaErrorInvalidValue) return SGM_ERR_INVALID_ARGUMENT;
     return SGM_ERR_CUDA;
 }
+
+// Entry-point prologue: the handle's device is current for the call (restored on return).
+#define FF_ENTRY(dev)                        \
+    sgm::DeviceGuard guard_(dev);            \
+    if (guard_.status != cudaSuccess) return ff_status(guard_.status);
 
 template <class T>
 cudaError_t ff_alloc(T **p, size_t count) {
@@ -174,7 +178,8 @@ sgm_status sgm_flow_create(const sgm_flow_params *p, int32_t device, sgm_flow_ha
     sgm_flow_handle *h = new sgm_flow_handle;
     h->prm = *p;
     h->device = device;
-    cudaError_t e = cudaSetDevice(device);
+    sgm::DeviceGuard guard(device);
+    cudaError_t e = guard.status;
     int W = p->width, H = p->height;
     long long off = 0;
     for (int l = 0; l < p->levels; ++l) {
@@ -215,7 +220,7 @@ sgm_status sgm_flow_create(const sgm_flow_params *p, int32_t device, sgm_flow_ha
 
 void sgm_flow_destroy(sgm_flow_handle *h) {
     if (!h) return;
-    cudaSetDevice(h->device);
+    sgm::DeviceGuard guard(h->device);
     cudaDeviceSynchronize();
     ff_free(h);
     delete h;
@@ -232,6 +237,7 @@ sgm_status sgm_flow_set_timing(sgm_flow_handle *h, int32_t enable) {
 
 int32_t sgm_flow_read_timing(sgm_flow_handle *h, float *ms) {
     if (!h || !ms || h->nev == 0) return 0;
+    sgm::DeviceGuard guard(h->device);
     for (int k = 0; k < SGM_FLOW_NUM_STAGES; ++k) ms[k] = 0.f;
     for (int i = 0; i < h->nev; i += 2) {
         float t = 0.f;
@@ -247,6 +253,7 @@ sgm_status sgm_flow_descriptors(sgm_flow_handle *h, const uint8_t *img, int32_t 
                                 int32_t *desc, void *stream) {
     if (!h || !img || !desc || w < 1 || hgt < 1) return SGM_ERR_INVALID_ARGUMENT;
     if ((reinterpret_cast<uintptr_t>(desc) & 15) != 0) return SGM_ERR_INVALID_ARGUMENT;
+    FF_ENTRY(h->device);
     cudaError_t e = sgm::ff_launch_wht(img, 0, w, hgt, h->prm.desc_window, 1, desc,
                                        static_cast<cudaStream_t>(stream));
     if (e == cudaSuccess) ++h->launches;
@@ -260,6 +267,7 @@ sgm_status sgm_flow_patch_cost(sgm_flow_handle *h, const uint8_t *A, const uint8
         return SGM_ERR_INVALID_ARGUMENT;
     if (nq == 0) return SGM_OK;
     if ((long long)w * hgt > h->lper[0]) return SGM_ERR_INVALID_ARGUMENT;
+    FF_ENTRY(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = sgm::ff_launch_quad(B, 0, w, hgt, 1, h->quad, 0, st);
     if (e == cudaSuccess)
@@ -275,6 +283,7 @@ sgm_status sgm_flow_knn_init(sgm_flow_handle *h, const uint8_t *A, const uint8_t
         return SGM_ERR_INVALID_ARGUMENT;
     const long long n = (long long)w * hgt;
     if (n > h->lper[0]) return SGM_ERR_INVALID_ARGUMENT;     // scratch sized for level 0
+    FF_ENTRY(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // images into the scratch pyramid slot 0 as one "pair" (A, B), level-0 layout
     cudaError_t e = cudaMemcpyAsync(h->pyr, A, size_t(n), cudaMemcpyDeviceToDevice, st);
@@ -300,6 +309,7 @@ sgm_status sgm_flow_sweep(sgm_flow_handle *h, const uint8_t *A, const uint8_t *B
         level < 0)
         return SGM_ERR_INVALID_ARGUMENT;
     if (hgt > h->prm.height || w > h->prm.width) return SGM_ERR_INVALID_ARGUMENT;
+    FF_ENTRY(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     sgm::FFFields F{};
     F.W = w; F.H = hgt; F.fpp = 1; F.nfields = 1;
@@ -318,6 +328,7 @@ sgm_status sgm_flow_sweep(sgm_flow_handle *h, const uint8_t *A, const uint8_t *B
 sgm_status sgm_flow_consistency(sgm_flow_handle *h, const int32_t *F, const int32_t *G1, const int32_t *G2,
                                 int32_t w, int32_t hgt, uint8_t *valid, void *stream) {
     if (!h || !F || !G1 || !G2 || !valid || w < 1 || hgt < 1) return SGM_ERR_INVALID_ARGUMENT;
+    FF_ENTRY(h->device);
     cudaError_t e = sgm::ff_launch_consistency(F, G1, G2, 0, 0, w, hgt, 1, h->prm.consistency_q, valid,
                                                nullptr, static_cast<cudaStream_t>(stream));
     if (e == cudaSuccess) ++h->launches;
@@ -328,6 +339,7 @@ sgm_status sgm_flow_field(sgm_flow_handle *h, int32_t n, const uint8_t *A, const
                           int32_t radius, int32_t *flow_q, int32_t *cost, void *stream) {
     if (!h || !A || !B || !flow_q || n < 1 || n > h->prm.max_batch || radius < 0 || radius + 2 > 7)
         return SGM_ERR_INVALID_ARGUMENT;
+    FF_ENTRY(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = upload_pairs(h, n, A, B, st, cudaMemcpyDeviceToDevice);
     int res = 0;
@@ -345,6 +357,7 @@ sgm_status sgm_flow(sgm_flow_handle *h, int32_t n, const uint8_t *frames0, const
     if (!h || !frames0 || !frames1 || n < 1 || n > h->prm.max_batch || (!flow && !valid && !fields_q))
         return SGM_ERR_INVALID_ARGUMENT;
     if (flow && (reinterpret_cast<uintptr_t>(flow) & 7)) return SGM_ERR_INVALID_ARGUMENT;
+    FF_ENTRY(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = upload_pairs(h, n, frames0, frames1, st, cudaMemcpyDeviceToDevice);
     int res = 0;
@@ -377,6 +390,13 @@ sgm_status sgm_densify(int32_t n, int32_t width, int32_t height, int32_t channel
     if (scratch && ((reinterpret_cast<uintptr_t>(scratch) & 15) ||
                     scratch_bytes < int64_t(sgm::densify_scratch_bytes(n, width, height))))
         return SGM_ERR_INVALID_ARGUMENT;
+    // handle-free: run on the device that owns `field`
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, field) != cudaSuccess || attr.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        return SGM_ERR_INVALID_ARGUMENT;
+    }
+    FF_ENTRY(attr.device);
     sgm::DensifyParams p{};
     p.n = n; p.W = width; p.H = height; p.C = channels; p.K = K; p.lambda = lambda;
     p.field = field; p.valid = valid; p.guide = guide; p.out = out; p.unfilled = unfilled;

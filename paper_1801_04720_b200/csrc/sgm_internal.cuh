@@ -49,8 +49,34 @@ struct SweepParams {
     int *fwd_done;            // [view] forward-sweep rows finished (the backward sweep's band 0
                               // starts a view once it reaches H: the two launches overlap)
     unsigned long long *trace; // debug: per (ticket, warp) {start ns, end ns, smid, 0} or null
-    int debug_flags;           // debug (env SGM_DEBUG_FLAGS): 1 = no inter-warp/band waits
+    int debug_flags;           // debug (env SGM_DEBUG_FLAGS / sgm_debug_set_flags): 1 = no
+                               // inter-warp/band waits, 2 = no band handoff, 4 = force the
+                               // bounded cross-CTA waits to time out (fault-reporting test)
     int one;                   // always 1 (opaque to the compiler: keeps adds on the FMA pipe)
+    int *err;                  // device fault word (mapped host memory) or null: a timed-out
+                               // cross-CTA wait stores its SGM_FAULT_* code here
+};
+
+// device fault codes written into SweepParams::err (reported by sgm_get_device_error)
+constexpr int kFaultFwdDone = 1;     // backward sweep: the view's forward sweep never completed
+constexpr int kFaultBandInput = 2;   // a band's predecessor never published its last row
+
+// Sets the calling thread's current device for the lifetime of the object and restores
+// the previous one (the library links a static cudart, whose current device is separate
+// from the caller's runtime; every entry point of a handle runs on the handle's device).
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t status = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); prev = -1; }
+        if (prev != dev) status = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard &) = delete;
+    DeviceGuard &operator=(const DeviceGuard &) = delete;
 };
 
 struct CensusParams {

@@ -305,18 +305,32 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     if (warp >= hb) return;                         // rows past the band
     const bool has_row_below = (warp < hb - 1) && !(p.debug_flags & 1);
     const int y = BWD ? (H - 1 - j) : j;
+    // Bounded cross-CTA waits: a wait that times out (a scheduling or logic error, or the
+    // debug flag 4) stores its fault code into p.err -- the next entry point of the handle
+    // then fails with SGM_ERR_CUDA -- and the row runs to completion without storing its
+    // disparities, so that every other warp's waits still complete.
+    const bool force_timeout = (p.debug_flags & 4) != 0;
+    const int spin_cap = force_timeout ? (1 << 8) : (1 << 25);
+    bool failed = false;
+    auto fault = [&](int code) {
+        failed = true;
+        if (p.err != nullptr && lane_id() == 0) *reinterpret_cast<volatile int *>(p.err) = code;
+    };
     if (BWD) {
         // the view's forward sweep must be complete before this row reads S_fwd (the
         // S_fwd prefetch below runs before any other synchronisation)
         // every lane polls (one request per poll): a lane-0-only loop made the compiler
         // treat the warp as possibly diverged and wrap every later SHFL / CREDUX in
         // WARPSYNC (backward sweep 3.36 -> 4.85 ms)
+        const int need = force_timeout ? H + 1 : H;
+        bool done = false;
 #pragma unroll 1
-        for (int spins = 0; spins < (1 << 26); ++spins) {
-            const bool done = ld_acquire_gpu(p.fwd_done + view) >= H;
-            if (__all_sync(0xffffffffu, done)) break;
+        for (int spins = 0; spins < 2 * spin_cap; ++spins) {
+            done = __all_sync(0xffffffffu, ld_acquire_gpu(p.fwd_done + view) >= need);
+            if (done) break;
             __nanosleep(256);
         }
+        if (!done) fault(kFaultFwdDone);
     }
 
     const uint64_t *ref, *match;
@@ -401,13 +415,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     auto issue_input = [&](int h) {
         const int q0 = h * G;
         if (q0 < W) {
-            const int need = min(q0 + G + 1, W);    // gbuf[q] is complete once q+1 is done
-            if (known < need) {
+            const int need = min(q0 + G + 1, W) + (force_timeout ? W : 0);   // gbuf[q] is
+            if (known < need) {                                      // complete once q+1 is done
                 int k, spins = 0;
                 // bounded wait: a logic error must not hang the GPU (~>2 s of polling)
-                while ((k = ld_relaxed_gpu(prog_in)) < need && ++spins < (1 << 25)) __nanosleep(32);
+                while ((k = ld_relaxed_gpu(prog_in)) < need && ++spins < spin_cap) __nanosleep(32);
                 asm volatile("fence.acq_rel.gpu;\n" ::: "memory");   // acquire what k covers
                 known = k;
+                if (__any_sync(0xffffffffu, k < need)) {             // timed out: stop waiting
+                    fault(kFaultBandInput);
+                    known = 1 << 30;
+                }
             }
             const char *g = reinterpret_cast<const char *>(gin + (long long)q0 * VEC) + 16 * lane;
 #pragma unroll 1
@@ -681,7 +699,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                     // every 32 positions each lane finishes one pixel: the parabola
                     // sub-pixel (one IEEE division per lane) and the stores
                     if (sl == 31 || i == W - 1) {
-                        if (lane <= sl) {
+                        if (lane <= sl && !failed) {
                             const int d = int(rec_key & 0xffu);
                             const int b = int(rec_key >> 8);
                             const int a = int(rec_ac & 0xffffu), c = int(rec_ac >> 16);

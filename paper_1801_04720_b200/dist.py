@@ -58,20 +58,57 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
-PACK_KEYS = ("sf", "valid_sf")
+# Per-rank result payload gathered to rank 0: S = (u, v, d0, d1) f32x4,
+# dP = (dX, dY, dZ, 0) f32x4 and the two masks -- 34 bytes per pixel, in this order.
+PACK_KEYS = ("sf", "dp", "valid_sf", "valid_3d")
+_PACK_FMT = {"sf": (torch.float32, 4), "dp": (torch.float32, 4), "valid_sf": (torch.uint8, 1),
+             "valid_3d": (torch.uint8, 1)}
+
+
+def packed_bytes(n: int, H: int, W: int) -> int:
+    return n * H * W * sum(torch.empty((), dtype=dt).element_size() * c for dt, c in _PACK_FMT.values())
+
+
+def _views(buf: torch.Tensor, n: int, H: int, W: int) -> dict:
+    out, off = {}, 0
+    for k in PACK_KEYS:
+        dt, c = _PACK_FMT[k]
+        nbytes = n * H * W * c * torch.empty((), dtype=dt).element_size()
+        v = buf[off:off + nbytes].view(dt)
+        out[k] = v.reshape(n, H, W, c) if c > 1 else v.reshape(n, H, W)
+        off += nbytes
+    return out
+
+
+def alloc_packed_outputs(sgm, n: int):
+    """One uint8 buffer per rank holding the gathered outputs, and the output dict of
+    sgm.scene_flow as views into it (S and dP 16-byte aligned), so the kernels write the
+    payload in place and the gather needs no packing copy."""
+    buf = torch.empty(packed_bytes(n, sgm.H, sgm.W), dtype=torch.uint8, device=sgm.device)
+    return buf, _views(buf, n, sgm.H, sgm.W)
 
 
 def pack_results(out: dict) -> torch.Tensor:
-    """Flatten the per-rank scene flow (S float32 [n][H][W][4] + mask) into one byte tensor."""
+    """Flatten a rank's results (PACK_KEYS order) into one byte tensor."""
     parts = [out[k].contiguous().view(torch.uint8).reshape(-1) for k in PACK_KEYS]
     return torch.cat(parts)
 
 
 def unpack_results(buf: torch.Tensor, n: int, H: int, W: int) -> dict:
-    sf_bytes = n * H * W * 4 * 4
-    sf = buf[:sf_bytes].view(torch.float32).reshape(n, H, W, 4)
-    v = buf[sf_bytes:sf_bytes + n * H * W].reshape(n, H, W)
-    return {"sf": sf, "valid_sf": v}
+    if buf.numel() != packed_bytes(n, H, W):
+        raise ValueError("packed buffer size does not match n x H x W")
+    return _views(buf, n, H, W)
+
+
+def gather_packed(buf: torch.Tensor, recv, rank: int, world: int):
+    """Gather every rank's packed buffer into rank 0's preallocated `recv` list (one
+    collective; NCCL with device tensors, gloo with host tensors)."""
+    if world <= 1:
+        return
+    if rank == 0:
+        dist.gather(buf, gather_list=recv, dst=0)
+    else:
+        dist.gather(buf, dst=0)
 
 
 def gather_results(out: dict, rank: int, world: int, device=None):
@@ -82,9 +119,6 @@ def gather_results(out: dict, rank: int, world: int, device=None):
         return [buf]
     if dist.get_backend() == "nccl":
         buf = buf.to(device)
-    if rank == 0:
-        bufs = [torch.empty_like(buf) for _ in range(world)]
-        dist.gather(buf, gather_list=bufs, dst=0)
-        return bufs
-    dist.gather(buf, dst=0)
-    return None
+    recv = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+    gather_packed(buf, recv, rank, world)
+    return recv

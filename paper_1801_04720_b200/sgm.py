@@ -84,6 +84,17 @@ class SGM:
     def launch_count(self) -> int:
         return int(self.lib.sgm_launch_count(self.h))
 
+    def device_error(self, clear: bool = False) -> int:
+        """Fault code of the handle's device fault word (0 = none); sgm_get_device_error.
+        Call after synchronising the stream of the call in question."""
+        code = ctypes.c_int32()
+        _lib.call("sgm_get_device_error", self.h, ctypes.byref(code), 1 if clear else 0)
+        return int(code.value)
+
+    def set_debug_flags(self, flags: int):
+        """sgm_debug_set_flags: 4 forces the sweeps' bounded waits to time out (tests)."""
+        _lib.call("sgm_debug_set_flags", self.h, int(flags))
+
     def set_timing(self, on: bool):
         _lib.call("sgm_set_timing", self.h, 1 if on else 0)
 

@@ -319,8 +319,22 @@ def video_quad(video: dict, k: int) -> dict:
             "gt_d1w": video["gt_d1w"][k], "gt_noc": video["gt_noc"][k]}
 
 
-def make_batch(cfg: Config | str, start: int, count: int) -> list:
-    return [make_quad(cfg, start + i) for i in range(count)]
+def make_batch(cfg: Config | str, start: int, count: int, workers: int = 1) -> list:
+    """Quads start .. start+count-1 of a config; `workers` > 1 generates them in a process
+    pool (forked, or spawned once CUDA is initialised in this process)."""
+    idx = [start + i for i in range(count)]
+    if workers <= 1 or count <= 1:
+        return [make_quad(cfg, i) for i in idx]
+    import multiprocessing as mp
+    method = "fork"
+    try:
+        import torch
+        if torch.cuda.is_initialized():
+            method = "spawn"
+    except Exception:  # pragma: no cover - torch is optional for the generator
+        pass
+    with mp.get_context(method).Pool(min(workers, count)) as pool:
+        return pool.starmap(make_quad, [(cfg, i) for i in idx])
 
 
 def manifest(quad: dict) -> dict:

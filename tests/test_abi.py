@@ -113,3 +113,23 @@ def test_flow_create_rejects_invalid_params(field, value):
     h = ctypes.c_void_p()
     assert lib.sgm_flow_create(ctypes.byref(p), 0, ctypes.byref(h)) == 1
     assert h.value is None
+
+
+@pytest.mark.parametrize("field,value", [("height", 65536), ("max_batch", 32768)])
+def test_create_rejects_launch_geometry_limits(field, value):
+    """Grid limits of the per-pixel kernels are refused at create time (UNSUPPORTED),
+    so no later call can fail half-way through its launch sequence."""
+    lib = _lib.load()
+    kw = dict(GOOD)
+    kw[field] = value
+    p = _lib.SgmParams(**kw)
+    h = ctypes.c_void_p()
+    assert lib.sgm_create(ctypes.byref(p), 0, ctypes.byref(h)) == 2
+    assert h.value is None
+
+
+def test_fault_and_debug_entry_points_reject_null():
+    lib = _lib.load()
+    code = ctypes.c_int32(-1)
+    assert lib.sgm_get_device_error(None, ctypes.byref(code), 0) == 1
+    assert lib.sgm_debug_set_flags(None, 4) == 1

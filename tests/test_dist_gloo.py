@@ -19,29 +19,46 @@ def _free_port():
     return port
 
 
+def _stamp(fidx, H, W):
+    """A stand-in per-quad "result" (no GPU needed): the frame index stamped into every
+    field of the payload."""
+    return {"sf": torch.full((H, W, 4), float(fidx)), "dp": torch.full((H, W, 4), -float(fidx)),
+            "valid_sf": torch.full((H, W), fidx % 2, dtype=torch.uint8),
+            "valid_3d": torch.full((H, W), (fidx + 1) % 2, dtype=torch.uint8)}
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     try:
         import torch.distributed as dist
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        per = 3
-        idx = sd.shard_indices(rank, world, per)
-        # a stand-in "result" per rank: frame indices stamped into S (no GPU needed)
-        n, H, W = per, 2, 3
-        sf = torch.zeros((n, H, W, 4), dtype=torch.float32)
-        for k, fidx in enumerate(idx):
-            sf[k] = float(fidx)
-        out = {"sf": sf, "valid_sf": torch.full((n, H, W), rank + 1, dtype=torch.uint8)}
+        total, H, W = 6, 2, 3
+        idx = sd.split_even(total, world, rank)       # configs[4]-style strong split
+        n = len(idx)
+        per = [_stamp(f, H, W) for f in idx]
+        out = {k: torch.stack([p[k] for p in per]) for k in sd.PACK_KEYS}
         t = sd.max_over_ranks(10.0 * (rank + 1))
         got = sd.gather_results(out, rank, world)
+        # the in-place variant: results written straight into the packed buffer
+        buf = torch.empty(sd.packed_bytes(n, H, W), dtype=torch.uint8)
+        views = sd.unpack_results(buf, n, H, W)
+        for k in sd.PACK_KEYS:
+            views[k].copy_(out[k])
+        recv = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+        sd.gather_packed(buf, recv, rank, world)
         res = {"rank": rank, "idx": idx, "tmax": t}
         if rank == 0:
             frames = []
-            for r, buf in enumerate(got):
-                u = sd.unpack_results(buf, n, H, W)
-                frames += [int(u["sf"][k, 0, 0, 0].item()) for k in range(n)]
-                assert int(u["valid_sf"][0, 0, 0]) == r + 1
+            for r in range(world):
+                assert torch.equal(got[r], recv[r])
+                u = sd.unpack_results(recv[r], n, H, W)
+                for k in range(n):
+                    fidx = int(u["sf"][k, 0, 0, 0].item())
+                    ref = _stamp(fidx, H, W)
+                    for key in sd.PACK_KEYS:
+                        assert torch.equal(u[key][k], ref[key]), (r, k, key)
+                    frames.append(fidx)
             res["frames"] = frames
         else:
             assert got is None
@@ -64,10 +81,32 @@ def test_shard_math():
 
 def test_pack_roundtrip():
     n, H, W = 2, 3, 5
-    sf = torch.randn(n, H, W, 4)
-    v = torch.randint(0, 2, (n, H, W), dtype=torch.uint8)
-    u = sd.unpack_results(sd.pack_results({"sf": sf, "valid_sf": v}), n, H, W)
-    assert torch.equal(u["sf"], sf) and torch.equal(u["valid_sf"], v)
+    out = {"sf": torch.randn(n, H, W, 4), "dp": torch.randn(n, H, W, 4),
+           "valid_sf": torch.randint(0, 2, (n, H, W), dtype=torch.uint8),
+           "valid_3d": torch.randint(0, 2, (n, H, W), dtype=torch.uint8)}
+    buf = sd.pack_results(out)
+    assert buf.numel() == sd.packed_bytes(n, H, W) == n * H * W * 34
+    u = sd.unpack_results(buf, n, H, W)
+    for k in sd.PACK_KEYS:
+        assert torch.equal(u[k], out[k]), k
+    with pytest.raises(ValueError):
+        sd.unpack_results(buf[:-1], n, H, W)
+
+
+def test_bench_refuses_world_mismatch():
+    """bench.py exits non-zero when WORLD_SIZE disagrees with --gpus, or when the 64-quad
+    batch does not split evenly, before touching any GPU."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "1"], env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "3"], env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and "split" in r.stderr
 
 
 def test_gloo_world2_gather_and_max():

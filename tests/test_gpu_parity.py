@@ -240,24 +240,41 @@ def test_scene_flow_full_size(orc, dev, name):
     g.close()
 
 
-def test_batch_config_sampled(orc, dev):
-    """configs[4]: 8 quads in one batched launch (the per-GPU shard at N=8); two
-    sampled quads checked element by element, all checked for determinism."""
+def oracle_many(orc, quads, prm):
+    """The oracle on every quad, one quad per host thread (ctypes releases the GIL)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    cores = len(os.sched_getaffinity(0))
+    with ThreadPoolExecutor(max_workers=max(1, min(cores, len(quads)))) as ex:
+        return list(ex.map(lambda q: orc.run_quad(q, prm, threads=False), quads))
+
+
+def check_quad_outputs(out, i, o):
+    """Every output field of quad i of a batched launch against the oracle's run_quad."""
+    for t, key in ((0, "disp0"), (1, "disp1")):
+        assert np.array_equal(_np(out["disp_valid"][i, t]), o[key]["valid"]), (i, key)
+        assert np.array_equal(_np(out["disp_int"][i, t]), o[key]["d_int"]), (i, key)
+        assert np.abs(_np(out["disp_sub"][i, t]) - o[key]["d_sub"]).max() <= SUB_TOL, (i, key)
+    r = {k: out[k][i] for k in ("sf", "valid_sf", "p0", "dp", "valid_3d")}
+    _check_sceneflow(r, o["sf"], o["valid_sf"], o["p0"], o["p1"], o["dp"], o["valid_3d"])
+
+
+def test_batch_config_full(orc, dev):
+    """configs[4]: 8 quads in one batched launch (the per-GPU shard at N=8, the bench's
+    band geometry), EVERY quad and every output field (integer and LR-checked
+    disparities, masks, S, P0, dP) element by element against the oracle, run on the
+    host cores in parallel; a quad alone gives the same bytes as inside the batch."""
     cfg = synth.CONFIGS["batch"]
     prm = synth.sgm_params(cfg)
     from paper_1801_04720_b200 import SGM, Camera, stack_quads
     g = SGM.from_config(cfg, max_batch=8)
-    quads = [synth.make_quad(cfg, i) for i in range(8)]
+    quads = synth.make_batch(cfg, 0, 8, workers=8)
     imgs, flow = stack_quads(quads, g.pitch, dev)
     cam = Camera(prm["f"], prm["B"], prm["cx"], prm["cy"])
     out = g.scene_flow(imgs, flow, cam)
     torch.cuda.synchronize()
-    for i in (0, 5):
-        o = orc.run_quad(quads[i], prm)
-        assert np.array_equal(_np(out["disp_int"][i, 0]), o["disp0"]["d_int"])
-        assert np.array_equal(_np(out["disp_valid"][i, 1]), o["disp1"]["valid"])
-        assert np.array_equal(_np(out["valid_sf"][i]), o["valid_sf"])
-    # the same quad alone gives the same bytes as inside the batch
+    for i, o in enumerate(oracle_many(orc, quads, prm)):
+        check_quad_outputs(out, i, o)
     g1 = SGM.from_config(cfg, max_batch=1)
     one = g1.scene_flow(imgs[5:6].contiguous(), flow[5:6].contiguous(), cam)
     torch.cuda.synchronize()
