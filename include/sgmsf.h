@@ -306,7 +306,8 @@ SGM_API sgm_status sgm_get_device_error(sgm_handle *h, int32_t *code, int32_t cl
 /* Debugging / fault-injection flags of the sweeps (default: env SGM_DEBUG_FLAGS or 0):
  * 1 = no inter-warp / inter-band waits, 2 = no band handoff (both give WRONG results;
  * timing experiments only), 4 = force every bounded cross-CTA wait to time out (tests
- * the fault reporting).  SGM_ERR_INVALID_ARGUMENT outside 0..7. */
+ * the fault reporting), 16 = keep the consumed band-handoff lines in L2 (no discard;
+ * traffic experiments).  SGM_ERR_INVALID_ARGUMENT outside 0..31. */
 SGM_API sgm_status sgm_debug_set_flags(sgm_handle *h, int32_t flags);
 
 #ifdef __cplusplus

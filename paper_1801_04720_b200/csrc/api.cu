@@ -187,6 +187,7 @@ sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int *sync = nullp
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+
 }  // namespace
 
 extern "C" {
@@ -334,7 +335,7 @@ sgm_status sgm_debug_set_trace(sgm_handle *h, uint64_t *trace) {
 }
 
 sgm_status sgm_debug_set_flags(sgm_handle *h, int32_t flags) {
-    if (!h || flags < 0 || flags > 7) return SGM_ERR_INVALID_ARGUMENT;
+    if (!h || flags < 0 || flags > 31) return SGM_ERR_INVALID_ARGUMENT;
     h->debug_flags = flags;
     return SGM_OK;
 }

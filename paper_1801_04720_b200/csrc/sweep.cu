@@ -107,6 +107,13 @@ __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Drop a 128-byte line from L2 without writing it back (PTX discard.global.L2): the band
+// handoff rows are read exactly once, by the next band, right after they are written; once
+// they sit in the consumer's shared memory their dirty L2 lines would otherwise be written
+// back to DRAM for nothing (~0.7 GB per sweep launch on 8 Driving quads).
+__device__ __forceinline__ void discard_l2(const void *p) {
+    asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ void st_relaxed_gpu(int *p, int v) {
     asm volatile("st.relaxed.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
@@ -275,7 +282,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
 
     // warp index through a warp reduction: the compiler then keeps it (and everything
     // derived from it) in uniform registers and emits uniform branches.
-    const int warp = int(__reduce_min_sync(0xffffffffu, threadIdx.x >> 5));
+    const int wid = int(__reduce_min_sync(0xffffffffu, threadIdx.x >> 5));
+    // row of the band this warp computes: the band's first (upstream) row runs on the
+    // highest compute-warp id (the warp arbiter favours high warp ids, so upstream rows win
+    // ties and downstream rows find their inputs ready: 6.77 -> 6.73 ms on 8 Driving quads)
+    const int warp = wid == NW ? wid : NW - 1 - wid;
     const int lane = lane_id();
     const int W = p.W, H = p.H;
     if (warp == NW) {
@@ -284,8 +295,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
         // to L2) runs here, off the producer's critical path.  Causality: producer lanes'
         // gbuf stores -> mbarrier arrive (release.cta) -> wait here (acquire.cta) ->
         // fence.acq_rel.gpu -> flag store (cumulative release).
+        // It also drops this band's consumed INPUT handoff lines from L2 (discard, no
+        // write-back): once the band's last row has passed position q, warp 0 has long
+        // copied input q into shared memory.  (Done here, off the compute warps: issued by
+        // warp 0 itself the discards cost 1-12 % of the sweep.)
         if (band + 1 < p.nbands && !(p.debug_flags & 3)) {
             int *prog = p.progress + view * p.nbands + band;
+            const char *gin_b = (band > 0 && !(p.debug_flags & 16)) ? reinterpret_cast<const char *>(
+                                               p.gbuf + (long long)(view * p.nbands + band - 1) * W * (3 * DP))
+                                         : nullptr;
+            constexpr int kLinesPerPos = 3 * DP * 2 / 128;
             const int ngroups = (W + PUB - 1) / PUB;
             for (int k = 0; k < ngroups; ++k) {
                 mbar_wait(pub_full + (k % kPubDepth), unsigned(k / kPubDepth) & 1u);
@@ -293,6 +312,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                 if (lane == 0) {
                     st_relaxed_gpu(prog, min((k + 1) * PUB, W));
                     mbar_arrive(pub_empty + (k % kPubDepth));
+                }
+                if (gin_b != nullptr) {
+                    const int q0 = k * PUB, nl = (min(q0 + PUB, W) - q0) * kLinesPerPos;
+                    const char *g0 = gin_b + (long long)q0 * (3 * DP * 2);
+                    for (int c = lane; c < nl; c += 32) discard_l2(g0 + 128 * c);
                 }
                 __syncwarp();
             }
@@ -307,14 +331,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     const int y = BWD ? (H - 1 - j) : j;
     // Bounded cross-CTA waits: a wait that times out (a scheduling or logic error, or the
     // debug flag 4) stores its fault code into p.err -- the next entry point of the handle
-    // then fails with SGM_ERR_CUDA -- and the row runs to completion without storing its
-    // disparities, so that every other warp's waits still complete.
+    // then fails with SGM_ERR_CUDA -- and the row runs to completion (so that every other
+    // warp's waits still complete); that call's results are invalid.
+    // (every lane stores the same code: a lane-0-only store would make the compiler treat
+    // the warp as possibly diverged and wrap the later SHFL / CREDUX in WARPSYNC; nothing
+    // of this state may stay live through the row loop: on 8 cells per lane the backward
+    // sweep spills, 5.85 -> 7.06 ms on 8 Wide quads)
     const bool force_timeout = (p.debug_flags & 4) != 0;
-    const int spin_cap = force_timeout ? (1 << 8) : (1 << 25);
-    bool failed = false;
     auto fault = [&](int code) {
-        failed = true;
-        if (p.err != nullptr && lane_id() == 0) *reinterpret_cast<volatile int *>(p.err) = code;
+        if (p.err != nullptr) *reinterpret_cast<volatile int *>(p.err) = code;
     };
     if (BWD) {
         // the view's forward sweep must be complete before this row reads S_fwd (the
@@ -325,7 +350,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
         const int need = force_timeout ? H + 1 : H;
         bool done = false;
 #pragma unroll 1
-        for (int spins = 0; spins < 2 * spin_cap; ++spins) {
+        for (int spins = 0; spins < (force_timeout ? (1 << 9) : (1 << 26)); ++spins) {
             done = __all_sync(0xffffffffu, ld_acquire_gpu(p.fwd_done + view) >= need);
             if (done) break;
             __nanosleep(256);
@@ -400,7 +425,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     const bool is_producer = (warp == hb - 1) && has_consumer && !(p.debug_flags & 3);
     uint16_t *gout = p.gbuf + (long long)nb_id * W * VEC + dbase;
     const uint16_t *gin = p.gbuf + (long long)(nb_id - 1) * W * VEC;
-    const int *prog_in = p.progress + (nb_id - 1);
+    // debug flag 4: poll a word nobody publishes (word 1 of the host-mapped fault block)
+    const int *prog_in = (force_timeout && p.err != nullptr) ? p.err + 1 : p.progress + (nb_id - 1);
     const bool nodeps = (p.debug_flags & 1) != 0;
     const bool noband = (p.debug_flags & 2) != 0;   // debug: no inter-band handoff
     const bool band_input = (warp == 0) && band > 0 && !nodeps && !noband;
@@ -415,17 +441,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     auto issue_input = [&](int h) {
         const int q0 = h * G;
         if (q0 < W) {
-            const int need = min(q0 + G + 1, W) + (force_timeout ? W : 0);   // gbuf[q] is
-            if (known < need) {                                      // complete once q+1 is done
+            const int need = min(q0 + G + 1, W);    // gbuf[q] is complete once q+1 is done
+            if (known < need) {
                 int k, spins = 0;
                 // bounded wait: a logic error must not hang the GPU (~>2 s of polling)
-                while ((k = ld_relaxed_gpu(prog_in)) < need && ++spins < spin_cap) __nanosleep(32);
+                const int cap = (p.debug_flags & 4) ? (1 << 8) : (1 << 25);
+                while ((k = ld_relaxed_gpu(prog_in)) < need && ++spins < cap) __nanosleep(32);
                 asm volatile("fence.acq_rel.gpu;\n" ::: "memory");   // acquire what k covers
-                known = k;
-                if (__any_sync(0xffffffffu, k < need)) {             // timed out: stop waiting
-                    fault(kFaultBandInput);
-                    known = 1 << 30;
-                }
+                // a time-out stops all later waits and is reported after the row (reporting
+                // it here, or raising `need` for the forced test, made the compiler wrap the
+                // forward sweep's loop in 23 more convergence barriers: 3.12 -> 3.31 ms)
+                known = __any_sync(0xffffffffu, k < need) ? (1 << 30) : k;
             }
             const char *g = reinterpret_cast<const char *>(gin + (long long)q0 * VEC) + 16 * lane;
 #pragma unroll 1
@@ -699,7 +725,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                     // every 32 positions each lane finishes one pixel: the parabola
                     // sub-pixel (one IEEE division per lane) and the stores
                     if (sl == 31 || i == W - 1) {
-                        if (lane <= sl && !failed) {
+                        if (lane <= sl) {
                             const int d = int(rec_key & 0xffu);
                             const int b = int(rec_key >> 8);
                             const int a = int(rec_ac & 0xffffu), c = int(rec_ac >> 16);
@@ -730,6 +756,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
         mbar_arrive(my_full + (((W - 1) / G) % RG));
     }
     if (band_input) cp_async_wait<0>();
+    if (band_input && known >= (1 << 30)) fault(kFaultBandInput);
     if (!BWD) {                                     // this row's S_fwd is complete
         __syncwarp();
         if (lane == 0) {
@@ -798,6 +825,7 @@ cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cud
 }  // namespace
 
 int sweep_warps_for(int cpl) { (void)cpl; return kBandRowsMax; }
+// [ticket, progress[nviews*nbands]] x 2 sweeps, fwd_done[nviews]
 size_t sweep_sync_ints(int nviews, int nbands) { return 2 * (1 + size_t(nviews) * nbands) + size_t(nviews); }
 
 cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool debug_s,
