@@ -70,25 +70,35 @@ SGM_API sgm_status sgm_flow(sgm_flow_handle *h, int32_t n, const uint8_t *frames
                     void *stream);
 
 /* ---- densification ------------------------------- */
-/* Edge-aware gap filling of a sparse field (SPEC densify S:253-262, F-6; the gap filling the
- * paper delegates to EpicFlow, and the "Ours (All)" densification):
- * a pixel with valid != 0 keeps its values exactly; a gap pixel p takes the mean of its K
- * nearest valid seeds s (squared Euclidean distance, ties to the smaller linear index)
- * weighted by 1 / (|p - s| + lambda * sum_k g(q_k)), q_k the interior points of the
- * segment p -> s (n = max(|dx|,|dy|) steps, rounded half up) and g the guide's L1
- * central-difference gradient (readings DN1-DN4).  No handle: plain device pointers.
+/* Edge-aware gap filling of a sparse field (SPEC densify S:253-262, decision F-6 "K-nearest
+ * seeds under edge-aware line-integral distance with inverse-distance weights"; the gap
+ * filling the paper delegates to EpicFlow, and the "Ours (All)" densification, P:147,
+ * P:170): a pixel with valid != 0 keeps its values exactly; a gap pixel p takes the
+ * 1/d_e-weighted mean of the K valid seeds s of smallest edge-aware distance
+ *   d_e(p, s) = |p - s| + lambda * sum_k g(q_k)
+ * (ties to the smaller linear index), q_k the interior points of the segment p -> s (n =
+ * max(|dx|,|dy|) steps, rounded half up) and g the guide's L1 central-difference gradient
+ * (readings DN1-DN4).  d_e is evaluated in fp64 as sqrt(|p-s|^2) + lambda * G, one rounding
+ * each: the seed choice is reproducible bit for bit.  Candidates: window <= 0 = every seed of
+ * the image (the SPEC's definition); window > 0 = the seeds within Chebyshev distance
+ * max(window, rho_K(p)), rho_K(p) the smallest Chebyshev radius holding K seeds (a bounded-
+ * cost approximation; pixels whose search provably found the window-0 answer -- the K-th d_e
+ * fell below the ring radius -- are counted in *certified).  No handle: plain device
+ * pointers, run on the device that owns `field`.
  *   field, out [n][H][W][C] float32 (C = 1..4: flow (u, v), scene flow (u, v, d0, d1), ...);
  *   valid, guide [n][H][W] uint8; 1 <= K <= 64; lambda >= 0 (gray levels -> px, 1.0);
  *   unfilled (device int32, nullable): number of pixels of images without any valid pixel
  *   (their output is 0, the SPEC's "zero valid pixels" error);
+ *   certified (device int32, nullable): gap pixels with a provably window-0 result;
  *   scratch: device, 16-byte aligned, scratch_bytes >= sgm_densify_scratch_bytes(n, W, H)
- *   (row / column prefix counts and the guide gradient); NULL = a stream-ordered allocation
- *   inside the call (slower, and not capturable in every CUDA-graph setting).
- * Arithmetic in float32. */
+ *   (row / column prefix counts, the gap list and the guide gradient); NULL = a stream-
+ *   ordered allocation inside the call (slower, and not capturable in every CUDA-graph
+ *   setting).  n * W * H < 2^31.
+ * Ranking and weights in fp64, output float32. */
 SGM_API sgm_status sgm_densify(int32_t n, int32_t width, int32_t height, int32_t channels,
                        const float *field, const uint8_t *valid, const uint8_t *guide,
-                       int32_t K, float lambda, float *out, int32_t *unfilled, void *scratch,
-                       int64_t scratch_bytes, void *stream);
+                       int32_t K, float lambda, int32_t window, float *out, int32_t *unfilled,
+                       int32_t *certified, void *scratch, int64_t scratch_bytes, void *stream);
 
 /* Scratch bytes sgm_densify needs for n images of width x height (-1 if invalid). */
 SGM_API int64_t sgm_densify_scratch_bytes(int32_t n, int32_t width, int32_t height);

@@ -350,18 +350,25 @@ int orc_ff_flow(const uint8_t *A, const uint8_t *B, int W, int H, int levels, in
 }
 
 /* ------------------------------------------------------------------ */
-/* Densification (SPEC densify S:253-262, F-6;  */
-/* the gap filling the paper delegates to EpicFlow, and the      */
-/* "Ours (All)" densification).  Readings DN1-DN4        */
-/* (DESIGN.md): a pixel with valid != 0 keeps its C values exactly; a  */
-/* gap pixel p takes the average of its K nearest valid seeds s (by    */
-/* squared Euclidean distance, ties to the smaller linear index)       */
-/* weighted by 1 / d_e(p, s), with the edge-aware distance             */
-/*   d_e = |p - s| + lambda * sum_k g(q_k),                             */
-/* q_k = the interior points of the segment p -> s (n = max(|dx|,|dy|) */
-/* steps, q_k = p + round-half-up(k (s - p) / n), k = 1..n-1) and      */
-/* g(q) = |G(x+1,y) - G(x-1,y)| + |G(x,y+1) - G(x,y-1)| (clamped).     */
-/* fp64.  An image with no valid pixel yields zeros (returns 3).       */
+/* Densification (SPEC densify S:253-262, F-6:   */
+/* "K-nearest seeds under edge-aware line-integral distance with        */
+/* inverse-distance weights"; the gap filling the paper   */
+/* delegates to EpicFlow, and the "Ours (All)" densification,     */
+/* P:147).  Readings DN1-DN4:                         */
+/*   d_e(p, s) = |p - s| + lambda * sum_k g(q_k)                         */
+/* with q_k = the interior points of the segment p -> s (n = max(|dx|,  */
+/* |dy|) steps, q_k = p + round-half-up(k (s - p) / n), k = 1..n-1) and */
+/* g(q) = |G(x+1,y) - G(x-1,y)| + |G(x,y+1) - G(x,y-1)| (clamped), G the */
+/* guide image.  A pixel with valid != 0 keeps its C values exactly; a  */
+/* gap pixel p takes the 1/d_e-weighted mean of the K valid seeds of    */
+/* smallest d_e (DN1: ties to the smaller linear index), d_e evaluated  */
+/* as sqrt((double)|p-s|^2) + (double)lambda * (double)sum (one rounding */
+/* each, so the ranking is reproducible bit for bit).  window <= 0:     */
+/* every seed of the image is a candidate (the SPEC's definition);      */
+/* window > 0: only seeds within Chebyshev distance                     */
+/* max(window, rho_K(p)) are, rho_K(p) = the smallest Chebyshev radius  */
+/* holding >= K seeds (the whole image if it has fewer).  An image with */
+/* no valid pixel yields zeros (returns 3).                             */
 /* ------------------------------------------------------------------ */
 static int grad_l1(const uint8_t *G, int W, int H, int x, int y)
 {
@@ -387,19 +394,40 @@ double orc_edge_distance(const uint8_t *G, int W, int H, int px, int py, int sx,
     return sqrt((double)dx * dx + (double)dy * dy) + lambda * (double)acc;
 }
 
-/* Densified value of one pixel (the body of orc_densify for a gap pixel). */
+static int cheb(int ax, int ay, int bx, int by)
+{
+    const int dx = ax > bx ? ax - bx : bx - ax, dy = ay > by ? ay - by : by - ay;
+    return dx > dy ? dx : dy;
+}
+
+/* Densified value of one gap pixel p = (px, py) (the body of orc_densify). */
 static void densify_pixel(const float *field, const uint8_t *valid, const uint8_t *guide, int W, int H, int C,
-                          int K, double lambda, int px, int py, double *o)
+                          int K, float lambda, int window, int px, int py, double *o)
 {
     const int64_t n = (int64_t)W * H;
-    long long bd[64];
+    /* candidate radius: the whole image, or max(window, rho_K(p)) */
+    int R = W > H ? W : H;
+    if (window > 0) {
+        int *hist = calloc((size_t)R + 1, sizeof(int));
+        for (int64_t q = 0; q < n; ++q)
+            if (valid[q]) hist[cheb((int)(q % W), (int)(q / W), px, py)]++;
+        int rho = R, seen = 0;
+        for (int r = 0; r <= R; ++r) {
+            seen += hist[r];
+            if (seen >= K) { rho = r; break; }
+        }
+        free(hist);
+        R = window > rho ? window : rho;
+    }
+    double bd[64];
     int64_t bi[64];
     int cnt = 0;
-    for (int64_t q = 0; q < n; ++q) {              /* exhaustive: the K nearest seeds */
+    for (int64_t q = 0; q < n; ++q) {              /* every candidate, ranked by (d_e, index) */
         if (!valid[q]) continue;
-        const long long dx = q % W - px, dy = q / W - py;
-        const long long d = dx * dx + dy * dy;
-        if (cnt < K || d < bd[cnt - 1]) {
+        const int sx = (int)(q % W), sy = (int)(q / W);
+        if (cheb(sx, sy, px, py) > R) continue;
+        const double d = orc_edge_distance(guide, W, H, px, py, sx, sy, (double)lambda);
+        if (cnt < K || d < bd[cnt - 1]) {          /* q ascends: equal d keeps the smaller index */
             int pos = cnt < K ? cnt++ : K - 1;
             while (pos > 0 && bd[pos - 1] > d) {
                 bd[pos] = bd[pos - 1];
@@ -412,8 +440,7 @@ static void densify_pixel(const float *field, const uint8_t *valid, const uint8_
     }
     double wsum = 0.0, acc[4] = {0, 0, 0, 0};
     for (int k = 0; k < cnt; ++k) {
-        const int sx = (int)(bi[k] % W), sy = (int)(bi[k] / W);
-        const double w = 1.0 / orc_edge_distance(guide, W, H, px, py, sx, sy, lambda);
+        const double w = 1.0 / bd[k];
         wsum += w;
         for (int c = 0; c < C; ++c) acc[c] += w * field[bi[k] * C + c];
     }
@@ -421,7 +448,7 @@ static void densify_pixel(const float *field, const uint8_t *valid, const uint8_
 }
 
 int orc_densify(const float *field, const uint8_t *valid, const uint8_t *guide, int W, int H, int C,
-                int K, double lambda, double *out)
+                int K, float lambda, int window, double *out)
 {
     if (K < 1 || K > 64 || C < 1 || C > 4) return 1;
     const int64_t n = (int64_t)W * H;
@@ -432,14 +459,14 @@ int orc_densify(const float *field, const uint8_t *valid, const uint8_t *guide, 
             for (int c = 0; c < C; ++c) out[p * C + c] = field[p * C + c];
             continue;
         }
-        densify_pixel(field, valid, guide, W, H, C, K, lambda, (int)(p % W), (int)(p / W), out + p * C);
+        densify_pixel(field, valid, guide, W, H, C, K, lambda, window, (int)(p % W), (int)(p / W), out + p * C);
     }
     return nseed == 0 ? 3 : 0;
 }
 
 /* The same at a list of pixels xy[npts][2] (for parity samples of full-size images). */
 int orc_densify_points(const float *field, const uint8_t *valid, const uint8_t *guide, int W, int H, int C,
-                       int K, double lambda, int npts, const int *xy, double *out)
+                       int K, float lambda, int window, int npts, const int *xy, double *out)
 {
     if (K < 1 || K > 64 || C < 1 || C > 4) return 1;
     for (int i = 0; i < npts; ++i) {
@@ -448,7 +475,7 @@ int orc_densify_points(const float *field, const uint8_t *valid, const uint8_t *
         if (valid[p]) {
             for (int c = 0; c < C; ++c) out[i * C + c] = field[p * C + c];
         } else {
-            densify_pixel(field, valid, guide, W, H, C, K, lambda, x, y, out + i * C);
+            densify_pixel(field, valid, guide, W, H, C, K, lambda, window, x, y, out + i * C);
         }
     }
     return 0;

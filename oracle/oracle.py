@@ -72,9 +72,10 @@ def _get():
             lib.orc_ff_flow.argtypes = [P, P, I, I, I, I, I, I, I, I, I, U64, I, P, P]
             lib.orc_edge_distance.argtypes = [P, I, I, I, I, I, I, Dd]
             lib.orc_edge_distance.restype = Dd
-            lib.orc_densify.argtypes = [P, P, P, I, I, I, I, Dd, P]
+            Fl = ctypes.c_float
+            lib.orc_densify.argtypes = [P, P, P, I, I, I, I, Fl, I, P]
             lib.orc_densify.restype = ctypes.c_int
-            lib.orc_densify_points.argtypes = [P, P, P, I, I, I, I, Dd, I, P, P]
+            lib.orc_densify_points.argtypes = [P, P, P, I, I, I, I, Fl, I, I, P, P]
             lib.orc_densify_points.restype = ctypes.c_int
             for fn in ("orc_ff_downsample", "orc_ff_wht", "orc_ff_knn_init", "orc_ff_sweep",
                        "orc_ff_lift", "orc_ff_field", "orc_ff_consistency", "orc_ff_flow"):
@@ -410,10 +411,12 @@ def edge_distance(guide, p, s, lam=1.0):
     return float(_get().orc_edge_distance(_p(guide), W, H, p[0], p[1], s[0], s[1], lam))
 
 
-def densify(field, valid, guide, K=25, lam=1.0):
+def densify(field, valid, guide, K=25, lam=1.0, window=0):
     """Fill the gaps of a C-channel field [H][W][C] (C <= 4): each gap pixel takes the
-    1/d_e-weighted mean of its K nearest valid seeds.  Returns float64 [H][W][C]; raises
-    if the image has no valid pixel (SPEC S:258 error)."""
+    1/d_e-weighted mean of its K valid seeds of smallest edge-aware distance d_e (SPEC
+    F-6); window > 0 restricts the candidates to Chebyshev distance max(window, rho_K).
+    lam is a float32 parameter (as in the C ABI).  Returns float64 [H][W][C]; raises if
+    the image has no valid pixel (SPEC S:258 error)."""
     field = _c(field, np.float32)
     if field.ndim == 2:
         field = field[..., None]
@@ -421,14 +424,14 @@ def densify(field, valid, guide, K=25, lam=1.0):
     guide = _c(guide, np.uint8)
     H, W, C = field.shape
     out = np.empty((H, W, C), np.float64)
-    rc = _get().orc_densify(_p(field), _p(valid), _p(guide), W, H, C, K, lam, _p(out))
+    rc = _get().orc_densify(_p(field), _p(valid), _p(guide), W, H, C, K, lam, window, _p(out))
     if rc == 3:
         raise ValueError("densify: no valid pixel")
     _chk(rc, "densify")
     return out
 
 
-def densify_points(field, valid, guide, xy, K=25, lam=1.0):
+def densify_points(field, valid, guide, xy, K=25, lam=1.0, window=0):
     """densify at the pixels xy [m][2] (x, y) only: float64 [m][C]."""
     field = _c(field, np.float32)
     if field.ndim == 2:
@@ -438,6 +441,6 @@ def densify_points(field, valid, guide, xy, K=25, lam=1.0):
     xy = _c(xy, np.int32)
     H, W, C = field.shape
     out = np.empty((len(xy), C), np.float64)
-    _chk(_get().orc_densify_points(_p(field), _p(valid), _p(guide), W, H, C, K, lam, len(xy), _p(xy),
-                                   _p(out)), "densify_points")
+    _chk(_get().orc_densify_points(_p(field), _p(valid), _p(guide), W, H, C, K, lam, window, len(xy),
+                                   _p(xy), _p(out)), "densify_points")
     return out

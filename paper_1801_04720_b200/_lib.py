@@ -147,7 +147,7 @@ def load(path: str | None = None):
         "sgm_flow_sweep": (st, [P, P, P, I32, I32, I32, I32, I32, ctypes.c_uint64, P, P, P]),
         "sgm_flow_consistency": (st, [P, P, P, P, I32, I32, P, P]),
         "sgm_flow_set_timing": (st, [P, I32]),
-        "sgm_densify": (st, [I32, I32, I32, I32, P, P, P, I32, ctypes.c_float, P, P, P, I64, P]),
+        "sgm_densify": (st, [I32, I32, I32, I32, P, P, P, I32, ctypes.c_float, I32, P, P, P, P, I64, P]),
         "sgm_densify_scratch_bytes": (I64, [I32, I32, I32]),
         "sgm_flow_read_timing": (I32, [P, ctypes.POINTER(ctypes.c_float)]),
     }

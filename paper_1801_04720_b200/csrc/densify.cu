@@ -1,16 +1,22 @@
 // densify.cu -- edge-aware densification of a sparse field (SPEC
-// densify S:253-262, F-6; the gap filling of P:87 and the "Ours (All)" densification of
-// P:147 / P:170).  Readings DN1-DN4: a gap pixel p takes the weighted mean of
-// its K nearest valid seeds (squared Euclidean distance, ties to the smaller linear index),
-// weight 1 / (|p - s| + lambda * sum of the guide's L1 central-difference gradient over the
-// interior points of the segment p -> s).
+// densify S:253-262, decision F-6 "K-nearest seeds under edge-aware line-integral distance
+// with inverse-distance weights"; the gap filling of P:87 and the "Ours (All)"
+// densification of P:147 / P:170).  Readings DN1-DN4: a gap pixel p takes the
+// 1/d_e-weighted mean of the K valid seeds of smallest edge-aware distance
+//   d_e(p, s) = |p - s| + lambda * sum of the guide's L1 central-difference gradient over
+//               the interior points of the segment p -> s
+// (ties to the smaller linear index), evaluated in fp64 exactly like the oracle
+// (sqrt(|p-s|^2) + lambda * G, one rounding each), so the seed choice is bit-identical.
+// window <= 0: every seed of the image competes (the SPEC's definition); window > 0: only
+// seeds within Chebyshev distance max(window, rho_K(p)), rho_K = the smallest Chebyshev
+// radius holding K seeds.
 //
-// One thread per pixel.  The K nearest seeds come from a ring search: rings of Chebyshev
-// radius r = 1, 2, ... are enumerated (sides without any valid pixel skipped in O(1) with
-// per-row / per-column prefix counts, so wide holes cost O(radius)) and offered to a
-// (distance^2 << 32 | index)-keyed top-K list; the search stops once K seeds are held and
-// r^2 exceeds the K-th distance^2 (every later pixel is at least r away), which is exactly
-// the exhaustive result.
+// One thread per gap pixel (gap pixels are compacted first; valid pixels are copied).  The
+// candidates are visited in rings of Chebyshev radius r = 1, 2, ... (ring sides without any
+// valid pixel skipped in O(1) with per-row / per-column prefix counts).  Exact pruning,
+// never changing the result: d_e >= |p - s| >= r, so a seed whose Euclidean distance exceeds
+// the current K-th d_e is not walked, and the search stops as soon as K seeds are held and
+// r exceeds the K-th d_e ("certified": the windowed result then equals the SPEC's).
 #include "sgm_internal.cuh"
 
 namespace sgm {
@@ -24,18 +30,21 @@ __device__ __forceinline__ int grad_l1(const uint8_t *__restrict__ G, int W, int
     return abs(gx) + abs(gy);
 }
 
+// top-K list ordered by (d_e, linear index)
 struct SeedList {
-    unsigned long long key[kDensifyKMax];   // (d^2 << 32) | linear index
+    double d[kDensifyKMax];
+    int idx[kDensifyKMax];
 };
 
-__device__ __noinline__ unsigned long long seed_insert(SeedList *L, int &cnt, int K, unsigned long long k) {
+__device__ __noinline__ void seed_insert(SeedList *L, int &cnt, int K, double d, int idx) {
     int pos = cnt < K ? cnt++ : K - 1;
-    while (pos > 0 && L->key[pos - 1] > k) {
-        L->key[pos] = L->key[pos - 1];
+    while (pos > 0 && (L->d[pos - 1] > d || (L->d[pos - 1] == d && L->idx[pos - 1] > idx))) {
+        L->d[pos] = L->d[pos - 1];
+        L->idx[pos] = L->idx[pos - 1];
         --pos;
     }
-    L->key[pos] = k;
-    return cnt == K ? L->key[K - 1] : ~0ull;
+    L->d[pos] = d;
+    L->idx[pos] = idx;
 }
 
 // Per-image prefix counts of valid pixels along rows (rowc[img][y][x] = #valid in row y,
@@ -88,29 +97,51 @@ struct RoundStep {
     }
 };
 
+// Valid pixels keep their values; gap pixels are appended to the gap list (warp-
+// aggregated: one atomic per warp, so a warp's gaps stay spatially together).
+__global__ void densify_split_kernel(const DensifyParams p, int *__restrict__ gaps, int *__restrict__ ngap) {
+    const long long total = (long long)p.W * p.H * p.n;
+    const int lane = threadIdx.x & 31;
+    for (long long base = (blockIdx.x * (long long)blockDim.x) & ~31ll; base < total;
+         base += (long long)gridDim.x * blockDim.x) {
+        const long long t = base + lane;
+        const bool in = t < total;
+        const bool gap = in && !p.valid[t];
+        if (in && !gap)
+            for (int c = 0; c < p.C; ++c) p.out[t * p.C + c] = p.field[t * p.C + c];
+        const unsigned m = __ballot_sync(0xffffffffu, gap);
+        int first = 0;
+        if (lane == 0 && m) first = atomicAdd(ngap, __popc(m));
+        first = __shfl_sync(0xffffffffu, first, 0);
+        if (gap) gaps[first + __popc(m & ((1u << lane) - 1))] = int(t);
+    }
+}
+
 __global__ void densify_kernel(const DensifyParams p, const int *__restrict__ rowc, const int *__restrict__ colc,
-                               const uint16_t *__restrict__ grad) {
-    const long long per = (long long)p.W * p.H, total = per * p.n;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
+                               const uint16_t *__restrict__ grad, const int *__restrict__ gaps,
+                               const int *__restrict__ ngap) {
+    const long long per = (long long)p.W * p.H;
+    const int n_gaps = *ngap;
+    const double lam = double(p.lambda);
+    const int rmax = max(p.W, p.H);
+    for (int gi = blockIdx.x * blockDim.x + threadIdx.x; gi < n_gaps; gi += gridDim.x * blockDim.x) {
+        const long long t = gaps[gi];
         const int img = int(t / per);
-        const long long q = t - img * per;
-        const int y = int(q / p.W), x = int(q - (long long)y * p.W);
+        const int q = int(t - img * per);
+        const int y = q / p.W, x = q - y * p.W;
         const uint8_t *valid = p.valid + img * per;
         const float *field = p.field + img * per * p.C;
+        const uint16_t *gimg = grad + img * per;
         float *out = p.out + t * p.C;
-        if (valid[q]) {
-            for (int c = 0; c < p.C; ++c) out[c] = field[q * p.C + c];
-            continue;
-        }
         SeedList L;
-        int cnt = 0;
-        unsigned long long kth = ~0ull;             // admission bound (K-th key once full)
-        const int rmax = max(p.W, p.H);
+        int cnt = 0, seen = 0, rho = -1;
+        bool certified = true;
         for (int r = 1; r <= rmax; ++r) {
-            if (cnt == p.K && (unsigned long long)r * r > (kth >> 32)) break;
-            // ring of Chebyshev radius r: rows y - r, y + r (full), columns x - r, x + r;
-            // each side is clipped to the image and skipped when its prefix count is zero
+            if (cnt == p.K && double(r) > L.d[p.K - 1]) break;                 // exact stop
+            if (p.window > 0 && rho >= 0 && r > max(p.window, rho)) {          // window stop
+                certified = false;
+                break;
+            }
             for (int side = 0; side < 4; ++side) {
                 int fixed, lo, hi;                  // the side's fixed coordinate and range
                 if (side < 2) {
@@ -128,38 +159,40 @@ __global__ void densify_kernel(const DensifyParams p, const int *__restrict__ ro
                 }
                 for (int k = lo; k <= hi; ++k) {
                     const int sx = side < 2 ? k : fixed, sy = side < 2 ? fixed : k;
-                    const long long sq = (long long)sy * p.W + sx;
+                    const int sq = sy * p.W + sx;
                     if (!valid[sq]) continue;
+                    ++seen;
                     const int dx = sx - x, dy = sy - y;
-                    const unsigned long long key = ((unsigned long long)(dx * dx + dy * dy) << 32) | unsigned(sq);
-                    if (key < kth) kth = seed_insert(&L, cnt, p.K, key);
+                    const double e = __dsqrt_rn(double(dx * dx + dy * dy));
+                    if (cnt == p.K && e > L.d[p.K - 1]) continue;          // d_e >= e: cannot enter
+                    const int n = max(abs(dx), abs(dy));
+                    int g = 0;
+                    RoundStep rx(dx, n), ry(dy, n);
+                    for (int j = 1; j < n; ++j) {
+                        const int qx = x + rx.next(), qy = y + ry.next();
+                        g += __ldg(gimg + qy * p.W + qx);
+                    }
+                    const double d = __dadd_rn(e, __dmul_rn(lam, double(g)));
+                    if (cnt < p.K || d < L.d[p.K - 1] || (d == L.d[p.K - 1] && sq < L.idx[p.K - 1]))
+                        seed_insert(&L, cnt, p.K, d, sq);
                 }
             }
-        }
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        float wsum = 0.f;
-        for (int k = 0; k < cnt; ++k) {
-            const int sq = int(L.key[k] & 0xffffffffu);
-            const int sy = sq / p.W, sx = sq - sy * p.W;
-            const int dx = sx - x, dy = sy - y;
-            const int n = max(abs(dx), abs(dy));
-            int g = 0;
-            RoundStep rx(dx, n), ry(dy, n);
-            const uint16_t *gi = grad + img * per;
-            for (int j = 1; j < n; ++j) {
-                const int qx = x + rx.next(), qy = y + ry.next();
-                g += __ldg(gi + (long long)qy * p.W + qx);
-            }
-            const float w = 1.0f / (sqrtf(float(dx * dx + dy * dy)) + p.lambda * float(g));
-            wsum += w;
-            for (int c = 0; c < p.C; ++c) acc[c] = fmaf(w, field[(long long)sq * p.C + c], acc[c]);
+            if (rho < 0 && seen >= p.K) rho = r;
         }
         if (cnt == 0) {
             for (int c = 0; c < p.C; ++c) out[c] = 0.f;
             if (p.unfilled) atomicAdd(p.unfilled, 1);
-        } else {
-            for (int c = 0; c < p.C; ++c) out[c] = acc[c] / wsum;
+            continue;
         }
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        double wsum = 0.0;
+        for (int k = 0; k < cnt; ++k) {
+            const double w = 1.0 / L.d[k];
+            wsum += w;
+            for (int c = 0; c < p.C; ++c) acc[c] += w * double(field[(long long)L.idx[k] * p.C + c]);
+        }
+        for (int c = 0; c < p.C; ++c) out[c] = float(acc[c] / wsum);
+        if (p.certified && certified) atomicAdd(p.certified, 1);
     }
 }
 
@@ -168,23 +201,27 @@ __global__ void densify_kernel(const DensifyParams p, const int *__restrict__ ro
 size_t densify_scratch_bytes(int n, int W, int H) {
     const size_t rown = size_t(n) * H * (W + 1), coln = size_t(n) * W * (H + 1);
     const size_t npx = size_t(n) * W * H;
-    return sizeof(int) * (rown + coln) + 2 * npx + 16;
+    // row / column prefix counts, gap list + its count (int), gradient image (uint16)
+    return sizeof(int) * (rown + coln + npx + 4) + 2 * npx + 16;
 }
 
 cudaError_t launch_densify(const DensifyParams &p, void *scratch_in, cudaStream_t st) {
     if (p.K < 1 || p.K > kDensifyKMax) return cudaErrorInvalidValue;
     cudaError_t e = cudaSuccess;
     if (p.unfilled) e = cudaMemsetAsync(p.unfilled, 0, sizeof(int), st);
-    // prefix counts + gradient image: caller scratch, else stream-ordered allocation
+    if (p.certified && e == cudaSuccess) e = cudaMemsetAsync(p.certified, 0, sizeof(int), st);
+    // prefix counts + gap list + gradient image: caller scratch, else stream-ordered allocation
     const size_t rown = size_t(p.n) * p.H * (p.W + 1), coln = size_t(p.n) * p.W * (p.H + 1);
+    const size_t npx = size_t(p.n) * p.W * p.H;
     int *scratch = reinterpret_cast<int *>(scratch_in);
     if (!scratch && e == cudaSuccess)
         e = cudaMallocAsync(reinterpret_cast<void **>(&scratch), densify_scratch_bytes(p.n, p.W, p.H), st);
     if (e != cudaSuccess) return e;
-    int *rowc = scratch, *colc = scratch + rown;
-    uint16_t *grad = reinterpret_cast<uint16_t *>(colc + coln);
-    densify_rowcount_kernel<<<(p.H * p.n + 127) / 128, 128, 0, st>>>(p, rowc);
-    e = cudaGetLastError();
+    int *rowc = scratch, *colc = scratch + rown, *gaps = colc + coln, *ngap = gaps + npx;
+    uint16_t *grad = reinterpret_cast<uint16_t *>(ngap + 4);
+    e = cudaMemsetAsync(ngap, 0, sizeof(int), st);
+    if (e == cudaSuccess) densify_rowcount_kernel<<<(p.H * p.n + 127) / 128, 128, 0, st>>>(p, rowc);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess) densify_colcount_kernel<<<(p.W * p.n + 127) / 128, 128, 0, st>>>(p, colc);
     if (e == cudaSuccess) e = cudaGetLastError();
     const long long total = (long long)p.W * p.H * p.n;
@@ -192,7 +229,10 @@ cudaError_t launch_densify(const DensifyParams &p, void *scratch_in, cudaStream_
     if (g > 148LL * 32) g = 148LL * 32;
     if (e == cudaSuccess) densify_grad_kernel<<<unsigned(g < 1 ? 1 : g), 128, 0, st>>>(p, grad);
     if (e == cudaSuccess) e = cudaGetLastError();
-    if (e == cudaSuccess) densify_kernel<<<unsigned(g < 1 ? 1 : g), 128, 0, st>>>(p, rowc, colc, grad);
+    if (e == cudaSuccess) densify_split_kernel<<<unsigned(g < 1 ? 1 : g), 128, 0, st>>>(p, gaps, ngap);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    // one thread per gap pixel; 64-thread blocks, a few waves of them per SM
+    if (e == cudaSuccess) densify_kernel<<<148 * 32, 64, 0, st>>>(p, rowc, colc, grad, gaps, ngap);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (!scratch_in) {
         const cudaError_t e2 = cudaFreeAsync(scratch, st);

@@ -27,6 +27,8 @@
 //   ff_consistency_kernel two-inverse-field check (thread per pixel)
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "sgm_internal.cuh"
 
 namespace sgm {
@@ -920,6 +922,8 @@ size_t ff_knn_scratch_bytes(long long entries) {
 cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int win, int32_t *nn, void *scratch,
                           cudaStream_t st) {
     if (knn < 1 || knn > kKnnMax) return cudaErrorInvalidValue;
+    static const bool legacy = getenv("SGM_KNN_MMA_SYNC") != nullptr;   // A/B experiments only
+    if (win <= 8 && !legacy) return ff_launch_knn_tc(desc, n, nprob, knn, nn, scratch, st);
     if (win <= 8) {                         // coefficients fit two exact limbs: tensor cores
         // every problem's query image and its partner database image (nprob may be odd: one
         // problem of a pair)

@@ -380,11 +380,13 @@ int64_t sgm_densify_scratch_bytes(int32_t n, int32_t width, int32_t height) {
 }
 
 sgm_status sgm_densify(int32_t n, int32_t width, int32_t height, int32_t channels, const float *field,
-                       const uint8_t *valid, const uint8_t *guide, int32_t K, float lambda, float *out,
-                       int32_t *unfilled, void *scratch, int64_t scratch_bytes, void *stream) {
+                       const uint8_t *valid, const uint8_t *guide, int32_t K, float lambda, int32_t window,
+                       float *out, int32_t *unfilled, int32_t *certified, void *scratch, int64_t scratch_bytes,
+                       void *stream) {
     if (n < 1 || width < 1 || height < 1 || width > 16384 || height > 16384 || channels < 1 || channels > 4 ||
         !field || !valid || !guide || !out || K < 1 || K > 64 || !(lambda >= 0.f))
         return SGM_ERR_INVALID_ARGUMENT;
+    if ((long long)n * width * height >= (1LL << 31)) return SGM_ERR_INVALID_ARGUMENT;
     if ((reinterpret_cast<uintptr_t>(field) & 3) || (reinterpret_cast<uintptr_t>(out) & 3))
         return SGM_ERR_INVALID_ARGUMENT;
     if (scratch && ((reinterpret_cast<uintptr_t>(scratch) & 15) ||
@@ -398,8 +400,9 @@ sgm_status sgm_densify(int32_t n, int32_t width, int32_t height, int32_t channel
     }
     FF_ENTRY(attr.device);
     sgm::DensifyParams p{};
-    p.n = n; p.W = width; p.H = height; p.C = channels; p.K = K; p.lambda = lambda;
+    p.n = n; p.W = width; p.H = height; p.C = channels; p.K = K; p.lambda = lambda; p.window = window;
     p.field = field; p.valid = valid; p.guide = guide; p.out = out; p.unfilled = unfilled;
+    p.certified = certified;
     return ff_status(sgm::launch_densify(p, scratch, static_cast<cudaStream_t>(stream)));
 }
 

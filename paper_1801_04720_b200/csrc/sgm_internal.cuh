@@ -128,10 +128,12 @@ struct FFFields {
 struct DensifyParams {
     int n, W, H, C, K;
     float lambda;
+    int window;                    // <= 0: every seed competes; > 0: Chebyshev max(window, rho_K)
     const float *field;            // [n][H][W][C]
     const uint8_t *valid, *guide;  // [n][H][W]
     float *out;                    // [n][H][W][C]
     int *unfilled;                 // nullable: pixels left without a seed
+    int *certified;                // nullable: gap pixels whose result provably equals window 0
 };
 
 // ----------------------------------------------------------------- launchers (host)
@@ -160,6 +162,8 @@ cudaError_t ff_launch_wht(const uint8_t *img, long long img_stride, int W, int H
 cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int win, int32_t *nn, void *scratch,
                           cudaStream_t st);
 size_t ff_knn_scratch_bytes(long long entries);
+cudaError_t ff_launch_knn_tc(const int32_t *desc, int n, int nprob, int knn, int32_t *nn, void *scratch,
+                             cudaStream_t st);
 cudaError_t ff_launch_init(const FFFields &F, const int32_t *nn, int knn, cudaStream_t st);
 cudaError_t ff_launch_lift(const FFFields &F, const int32_t *coarse, int Wc, int Hc, cudaStream_t st);
 // stage timer of the flow handle (flow_api.cu): begin(category) / end() around a launch

@@ -123,13 +123,18 @@ class FlowFields:
 
 
 _densify_scratch = {}
+# default candidate window of sgm_densify (Chebyshev px; 0 = every seed, the SPEC's F-6)
+DENSIFY_WINDOW = 16
 
 
-def densify(field, valid, guide, K=25, lam=1.0, stream=None, count_unfilled=False, scratch=None):
-    """Edge-aware densification (sgm_densify): field float32 [n][H][W][C] (or [H][W][C]),
-    valid / guide uint8 [n][H][W] (device).  Returns the dense field (and the number of
-    pixels of images without seeds if asked).  The scratch buffer is cached per shape and
-    device unless one is passed."""
+def densify(field, valid, guide, K=25, lam=1.0, window=DENSIFY_WINDOW, stream=None, count_unfilled=False,
+            count_certified=False, scratch=None):
+    """Edge-aware densification (sgm_densify, SPEC F-6): field float32 [n][H][W][C] (or
+    [H][W][C]), valid / guide uint8 [n][H][W] (device).  window = 0: every seed competes
+    (the SPEC's definition); > 0: seeds within Chebyshev max(window, rho_K).  Returns the
+    dense field, plus the number of pixels of images without seeds and / or the number of
+    gap pixels with a provably window-0 result if asked.  The scratch buffer is cached per
+    shape and device unless one is passed."""
     squeeze = field.dim() == 3
     if squeeze:
         field, valid, guide = field[None], valid[None], guide[None]
@@ -137,6 +142,7 @@ def densify(field, valid, guide, K=25, lam=1.0, stream=None, count_unfilled=Fals
     n, H, W, C = field.shape
     out = torch.empty_like(field)
     cnt = torch.zeros((1,), dtype=torch.int32, device=field.device) if count_unfilled else None
+    cert = torch.zeros((1,), dtype=torch.int32, device=field.device) if count_certified else None
     nbytes = int(_lib.load().sgm_densify_scratch_bytes(n, W, H))
     if scratch is None:
         key = (field.device, n, W, H)
@@ -145,6 +151,8 @@ def densify(field, valid, guide, K=25, lam=1.0, stream=None, count_unfilled=Fals
             scratch = torch.empty((nbytes,), dtype=torch.uint8, device=field.device)
             _densify_scratch[key] = scratch
     _lib.call("sgm_densify", n, W, H, C, _ptr(field), _ptr(valid.contiguous()), _ptr(guide.contiguous()),
-              int(K), float(lam), _ptr(out), _ptr(cnt), _ptr(scratch), nbytes, _stream(stream))
+              int(K), float(lam), int(window), _ptr(out), _ptr(cnt), _ptr(cert), _ptr(scratch), nbytes,
+              _stream(stream))
     out = out[0] if squeeze else out
-    return (out, cnt) if count_unfilled else out
+    res = (out,) + ((cnt,) if count_unfilled else ()) + ((cert,) if count_certified else ())
+    return res[0] if len(res) == 1 else res

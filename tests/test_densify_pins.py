@@ -72,10 +72,13 @@ def test_invariants(orc):
     assert np.allclose(orc.densify(const, v, g)[..., 0], 4.5, atol=1e-12)
 
 
-def _py_densify(f, v, g, K, lam):
-    """Independent re-implementation: numpy lexsort for the K nearest, explicit walk."""
+def _py_densify(f, v, g, K, lam, window=0):
+    """Independent re-implementation of SPEC F-6: every candidate seed's
+    edge-aware distance by an explicit walk, the K smallest by numpy lexsort (ties to the
+    smaller index), inverse-distance weights."""
     H, W, C = f.shape
     f = f.astype(np.float64)
+    lam = float(np.float32(lam))                      # the ABI's float32 parameter
     seeds = np.flatnonzero(v.reshape(-1))
     sy, sx = seeds // W, seeds % W
     out = f.astype(np.float64).copy()
@@ -89,19 +92,26 @@ def _py_densify(f, v, g, K, lam):
         for x in range(W):
             if v[y, x]:
                 continue
-            d2 = (sx - x) ** 2 + (sy - y) ** 2
-            order = np.lexsort((seeds, d2))[:K]
-            wsum, acc = 0.0, np.zeros(C)
-            for q in order:
+            ch = np.maximum(np.abs(sx - x), np.abs(sy - y))
+            if window > 0:
+                counts = np.bincount(ch, minlength=max(W, H) + 1).cumsum()
+                rho = int(np.argmax(counts >= K)) if counts[-1] >= K else max(W, H)
+                cand = np.flatnonzero(ch <= max(window, rho))
+            else:
+                cand = np.arange(len(seeds))
+            de = []
+            for q in cand:
                 dx, dy = int(sx[q] - x), int(sy[q] - y)
                 n = max(abs(dx), abs(dy))
                 s = 0
                 for k in range(1, n):
                     s += grad(x + math.floor(k * dx / n + 0.5), y + math.floor(k * dy / n + 0.5))
-                w = 1.0 / (math.hypot(dx, dy) + lam * s)
-                wsum += w
-                acc += w * f[sy[q], sx[q]]
-            out[y, x] = acc / wsum
+                de.append(math.sqrt(dx * dx + dy * dy) + lam * s)
+            de = np.array(de)
+            order = cand[np.lexsort((seeds[cand], de))][:K]
+            dsel = de[np.lexsort((seeds[cand], de))][:K]
+            w = 1.0 / dsel
+            out[y, x] = (w[:, None] * f[sy[order], sx[order]]).sum(0) / w.sum()
     return out
 
 
@@ -116,6 +126,47 @@ def test_brute_force(orc, seed):
     out = orc.densify(f, v, g, K=5, lam=0.7)
     ref = _py_densify(f, v, g, 5, 0.7)
     assert np.allclose(out, ref, rtol=1e-12, atol=1e-12)
+    outw = orc.densify(f, v, g, K=3, lam=0.7, window=2)
+    refw = _py_densify(f, v, g, 3, 0.7, window=2)
+    assert np.allclose(outw, refw, rtol=1e-12, atol=1e-12)
+
+
+def test_edge_aware_ranking_not_euclidean(orc):
+    """SPEC F-6 ranks seeds by the edge-aware distance, not by Euclidean distance: with
+    K = 1, a gap pixel next to a strong edge takes the farther seed on its own side
+    (d_e = 6) over the nearer one across the edge (d_e = 2 + 255)."""
+    H, W = 5, 20
+    g = np.zeros((H, W), np.uint8)
+    g[:, 11:] = 255                                      # edge between x = 10 and x = 11
+    f = np.zeros((H, W, 1), np.float32)
+    v = np.zeros((H, W), np.uint8)
+    v[2, 12], f[2, 12] = 1, 7.0                          # across the edge, |p - s| = 2
+    v[2, 4], f[2, 4] = 1, -3.0                           # same side, |p - s| = 6
+    out = orc.densify(f, v, g, K=1)
+    assert out[2, 10, 0] == -3.0
+    assert orc.edge_distance(g, (10, 2), (12, 2)) == pytest.approx(2.0 + 255)   # interior x = 11: g = 255
+    assert orc.edge_distance(g, (10, 2), (4, 2)) == pytest.approx(6.0)          # interior x = 9..5: g = 0
+    # both weights enter with K = 2: the closer-by-d_e seed dominates
+    out2 = orc.densify(f, v, g, K=2)
+    w_a, w_b = 1 / 6.0, 1 / (2.0 + 255)
+    assert out2[2, 10, 0] == pytest.approx((w_a * -3.0 + w_b * 7.0) / (w_a + w_b), rel=1e-12)
+
+
+def test_window_restricts_candidates(orc):
+    """window > 0: only seeds within Chebyshev distance max(window, rho_K) compete."""
+    H, W = 3, 30
+    g = np.full((H, W), 50, np.uint8)                    # flat guide: d_e = Euclidean
+    f = np.zeros((H, W, 1), np.float32)
+    v = np.zeros((H, W), np.uint8)
+    v[1, 0], f[1, 0] = 1, 1.0
+    v[1, 29], f[1, 29] = 1, 2.0
+    full = orc.densify(f, v, g, K=2)
+    x = 3                                                # distances 3 and 26
+    assert full[1, x, 0] == pytest.approx((1 / 3 * 1.0 + 1 / 26 * 2.0) / (1 / 3 + 1 / 26), rel=1e-12)
+    win = orc.densify(f, v, g, K=2, window=5)            # rho_2 = 26 at x = 3: both still in
+    assert win[1, x, 0] == full[1, x, 0]
+    win1 = orc.densify(f, v, g, K=1, window=5)           # rho_1 = 3: the far seed is out
+    assert win1[1, x, 0] == 1.0
 
 
 def test_no_seed_is_an_error(orc):

@@ -1,7 +1,8 @@
-"""GPU parity of the densification: sgm_densify against
-oracle.densify on the same seeded inputs.  The seed selection is exact (integer keys);
-the weighted means are float32 on the GPU and fp64 in the oracle: within
-1e-4 * max(1, |value|)."""
+"""GPU parity of the densification (SPEC F-6): sgm_densify against
+oracle.densify on the same seeded inputs, with every seed competing (window 0, the SPEC's
+definition) and with a candidate window.  The seed ranking is bit-reproducible (fp64 keys
+with one rounding each on both sides); the outputs are float32 on the GPU, fp64 in the
+oracle: within 1e-4 * max(1, |value|)."""
 import numpy as np
 import pytest
 import torch
@@ -35,13 +36,17 @@ def test_densify_parity(orc, dev, case):
     v = (rng.random((n, H, W)) < dens).astype(np.uint8)
     v[:, 0, 0] = 1
     g = np.stack([synth.translated_pair(W, H, k, 0, 0)[0] for k in range(n)])
-    out = densify(torch.from_numpy(f).to(dev), torch.from_numpy(v).to(dev), torch.from_numpy(g).to(dev),
-                  K=K, lam=lam).cpu().numpy()
-    for i in range(n):
-        ref = orc.densify(f[i], v[i], g[i], K=K, lam=lam)
-        m = v[i] > 0
-        assert np.array_equal(out[i][m], f[i][m])           # seeds kept bit for bit
-        assert _close(out[i], ref)
+    T = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
+    for window in (0, 3):
+        out, cert = densify(T(f), T(v), T(g), K=K, lam=lam, window=window, count_certified=True)
+        out = out.cpu().numpy()
+        for i in range(n):
+            ref = orc.densify(f[i], v[i], g[i], K=K, lam=lam, window=window)
+            m = v[i] > 0
+            assert np.array_equal(out[i][m], f[i][m])           # seeds kept bit for bit
+            assert _close(out[i], ref), window
+        if window == 0:                                         # every gap pixel is exact
+            assert int(cert.item()) == int((v == 0).sum())
 
 
 def test_densify_spec_examples_and_no_seed(dev):
@@ -70,14 +75,17 @@ def test_densify_estimated_flow_full_size(orc, dev):
     A = torch.from_numpy(q["il0"][None]).to(dev)
     B = torch.from_numpy(q["il1"][None]).to(dev)
     fo = ff.flow(A, B)
-    dense = densify(fo["flow"], fo["valid"], A).cpu().numpy()[0]
+    dense, cert = densify(fo["flow"], fo["valid"], A, count_certified=True)
+    dense = dense.cpu().numpy()[0]
     flow = fo["flow"].cpu().numpy()[0]
     valid = fo["valid"].cpu().numpy()[0]
     gaps = np.argwhere(valid == 0)
     rng = np.random.default_rng(0)
     pick = gaps[rng.choice(len(gaps), 150, replace=False)]
     xy = np.stack([pick[:, 1], pick[:, 0]], 1)
-    ref = orc.densify_points(flow, valid, q["il0"], xy)
+    from paper_1801_04720_b200.flow import DENSIFY_WINDOW
+    ref = orc.densify_points(flow, valid, q["il0"], xy, window=DENSIFY_WINDOW)
     assert _close(dense[pick[:, 0], pick[:, 1]], ref)
     assert np.array_equal(dense[valid > 0], flow[valid > 0])
+    assert 0 <= int(cert.item()) <= len(gaps)
     ff.close()

@@ -3,7 +3,7 @@
 (tools/profile_r02.sh) -> profiles/ncu_traffic.json ({"<config>/<kernel>": {"bytes",
 "quads", ...}}, read by bench.py for roofline.traffic) and a markdown summary.
 
-    python tools/ncu_traffic.py gpurun_out/r02_sweep_*.ncu-rep > profiles/r02_sweep_ncu.md
+    python tools/ncu_traffic.py gpurun_out/r02_sweep_*.raw.csv > profiles/r02_sweep_ncu.md
 """
 import csv
 import io
@@ -25,9 +25,15 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "u
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    """Raw page of a report (.ncu-rep) or of its saved CSV (.raw.csv)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
+    while rows and (not rows[0] or rows[0][0] != "ID" and "Kernel Name" not in rows[0]):
+        rows = rows[1:]
     return rows[0], rows[1], rows[2:]
 
 
@@ -44,7 +50,7 @@ def main(reps):
     sys.path.insert(0, ROOT)
     import synth
     for rep in reps:
-        m = re.search(r"sweep_(\w+?)x(\d+)\.ncu-rep$", rep)
+        m = re.search(r"sweep_(\w+?)x(\d+)\.(ncu-rep|raw\.csv)$", rep)
         cfgname, quads = m.group(1), int(m.group(2))
         cfg = synth.CONFIGS[cfgname]
         hdr, units, rows = raw(rep)
