@@ -46,7 +46,9 @@ class SgmError(RuntimeError):
             try:
                 msg += ": " + lib.sgm_status_string(code).decode()
                 if code == 3:
-                    msg += " (" + lib.sgm_last_error_string().decode() + ")"
+                    err = lib.sgm_flow_last_error_string if fn.startswith(("sgm_flow", "sgm_densify")) \
+                        else lib.sgm_last_error_string
+                    msg += " (" + err().decode() + ")"
             except Exception:  # pragma: no cover
                 pass
         super().__init__(f"{fn} failed: {msg}")

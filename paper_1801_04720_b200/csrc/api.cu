@@ -187,6 +187,11 @@ sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int *sync = nullp
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Both sweeps of a call (sweep.cu).
+cudaError_t run_sweeps(const sgm::SweepParams &p, int cpl, bool c64, int nw, bool debug_s, cudaStream_t st,
+                       cudaEvent_t mid_a, cudaEvent_t mid_b, int *launches) {
+    return sgm::launch_sweeps(p, cpl, c64, nw, debug_s, st, mid_a, mid_b, launches);
+}
 
 }  // namespace
 
@@ -411,7 +416,7 @@ sgm_status sgm_aggregate(sgm_handle *h, const uint64_t *cen_left, const uint64_t
     p.dsub = nullptr;
     p.sout = agg;
     int n = 0;
-    cudaError_t e = sgm::launch_sweeps(p, h->cpl, h->c64, h->nw, true,
+    cudaError_t e = run_sweeps(p, h->cpl, h->c64, h->nw, true,
                                        static_cast<cudaStream_t>(stream), nullptr, nullptr, &n);
     h->launches += n;
     return from_cuda(e);
@@ -464,7 +469,7 @@ sgm_status sgm_disparity(sgm_handle *h, const uint8_t *left, const uint8_t *righ
         ++h->launches;
         sgm::SweepParams p = sweep_params(h, 2);
         int n = 0;
-        e = sgm::launch_sweeps(p, h->cpl, h->c64, h->nw, false, st, nullptr, nullptr, &n);
+        e = run_sweeps(p, h->cpl, h->c64, h->nw, false, st, nullptr, nullptr, &n);
         h->launches += n;
     }
     if (e == cudaSuccess) {
@@ -563,7 +568,7 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, bool stream, const u
     {
         sgm::SweepParams p = sweep_params(h, 2 * npairs, sync);
         int nl = 0;
-        e = sgm::launch_sweeps(p, h->cpl, h->c64, h->nw, false, st, timing ? h->ev[2] : nullptr,
+        e = run_sweeps(p, h->cpl, h->c64, h->nw, false, st, timing ? h->ev[2] : nullptr,
                                nullptr, &nl);
         h->launches += nl;
         if (e != cudaSuccess) return from_cuda(e);

@@ -102,7 +102,7 @@ struct RoundStep {
 __global__ void densify_split_kernel(const DensifyParams p, int *__restrict__ gaps, int *__restrict__ ngap) {
     const long long total = (long long)p.W * p.H * p.n;
     const int lane = threadIdx.x & 31;
-    for (long long base = (blockIdx.x * (long long)blockDim.x) & ~31ll; base < total;
+    for (long long base = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31u); base < total;
          base += (long long)gridDim.x * blockDim.x) {
         const long long t = base + lane;
         const bool in = t < total;

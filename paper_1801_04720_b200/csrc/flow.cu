@@ -9,9 +9,11 @@
 // Kernels
 //   ff_downsample_kernel  2x2 box pyramid level (thread per output pixel)
 //   ff_wht_kernel         16 lowest-sequency WHT coefficients (thread per pixel)
-//   ff_knn_kernel         exhaustive k nearest descriptors (thread per query; the database
-//                         streams through shared memory in tiles; strict-< insertion in
-//                         index order reproduces the "ties to the smaller index" rule)
+//   ff_knn_kernel         exhaustive k nearest descriptors of the 16x16 window (thread per
+//                         query; the database streams through shared memory in tiles;
+//                         strict-< insertion in index order reproduces the "ties to the
+//                         smaller index" rule); windows up to 8x8 run on the tensor cores
+//                         (knn_tc.cu: tcgen05.mma into TMEM, exact limb arithmetic)
 //   ff_init_kernel        best of the k candidates by data term (thread per pixel)
 //   ff_prop_kernel        one propagation sweep: a persistent wavefront, one warp per
 //                         image row, the row's pixels in scan order; the warp's 32 lanes
@@ -25,10 +27,6 @@
 //                         propagation is done its warp searches the row (lane per pixel)
 //   ff_lift_kernel        x2 vectors, nearest-neighbour upsampling, costs recomputed
 //   ff_consistency_kernel two-inverse-field check (thread per pixel)
-#include <cuda_fp16.h>
-
-#include <cstdlib>
-
 #include "sgm_internal.cuh"
 
 namespace sgm {
@@ -284,270 +282,6 @@ __global__ void __launch_bounds__(128) ff_knn_kernel(const int32_t *__restrict__
     if (active)
         for (int k = 0; k < knn; ++k) nn[((long long)prob * n + qi) * knn + k] = bi[k];
 }
-
-// kNN on the tensor cores (window <= 8: |coefficient| <= 64 * 255 = 16320).  Every
-// coefficient splits exactly into limbs c = 128 h + l (h in [-128, 127], l in [0, 127]),
-// so the query . database dot product is
-//   q.b = 16384 sum(qh bh) + 128 sum(qh bl + ql bh) + sum(ql bl),
-// four m16n8k16 MMAs per 16 x 8 tile.  The epilogue forms the exact distance
-// |q|^2 + |b|^2 - 2 q.b in 64-bit integers where needed and keeps a (distance,
-// index)-ordered top-k per query row; the 4 lanes holding a row merge their lists at the
-// end.
-constexpr int kMmaTile = 128;             // database entries per shared-memory tile
-
-// (distance, index)-ordered k-best list in local memory (insertions are rare once it has
-// filled); the caller keeps the admission threshold (k-th entry) in registers.
-struct KList {
-    long long d[kKnnMax];
-    int i[kKnnMax];
-};
-
-__device__ __forceinline__ void klist_init(KList &L) {
-    for (int k = 0; k < kKnnMax; ++k) { L.d[k] = 0x7fffffffffffffffll; L.i[k] = 0x7fffffff; }
-}
-
-// insert (dv, ci) and return the list's new k-th entry; the caller keeps the tighter of
-// that and any bound it already had (a bound shared from other lists stays valid)
-__device__ __noinline__ long long klist_insert(KList *L, long long dv, int ci, int knn, int *thr_i) {
-    bool ins = false;
-    for (int k = 0; k < knn; ++k) {
-        if (ins || dv < L->d[k] || (dv == L->d[k] && ci < L->i[k])) {
-            const long long td = L->d[k]; const int ti = L->i[k];
-            L->d[k] = dv; L->i[k] = ci; dv = td; ci = ti;
-            ins = true;
-        }
-    }
-    *thr_i = L->i[knn - 1];
-    return L->d[knn - 1];
-}
-
-#define KOFFER(L, thr, thr_i, dv, ci)                                          \
-    do {                                                                       \
-        const long long dv_ = (dv);                                            \
-        const int ci_ = (ci);                                                  \
-        if (dv_ < thr || (dv_ == thr && ci_ < thr_i)) {                        \
-            int ti_;                                                           \
-            const long long t_ = klist_insert(&L, dv_, ci_, knn, &ti_);       \
-            if (t_ < thr || (t_ == thr && ti_ < thr_i)) { thr = t_; thr_i = ti_; } \
-        }                                                                      \
-    } while (0)
-
-// fp16 variant of the same exact decomposition: the limbs (|h| <= 128, l <= 127) are exact
-// fp16 values, every product is < 2^14 and every partial sum of 16 or 32 of them < 2^24,
-// so the fp32 accumulators hold the exact integers.  The epilogue first rejects in fp32
-// (error < 2^13 against a 2^15 margin) and forms the exact 64-bit distance only for the
-// rare entries within the margin of the admission bound.
-__device__ __forceinline__ void mma_f16(float (&c)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};\n"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ unsigned half2_bits(int lo, int hi) {
-    const __half2 v = __floats2half2_rn(float(lo), float(hi));
-    return *reinterpret_cast<const unsigned *>(&v);
-}
-
-// Packed database entry (64 B + norms): limbs of the 16 coefficients as half2 words,
-// word w = dims (2w, 2w+1), stored in the order w = 0, 4, 1, 5, 2, 6, 3, 7 so that the two
-// words a fragment lane t needs (w = t and t + 4) are one 64-bit load; computed once per
-// image by ff_knn_prep_kernel.
-struct KnnEntry {
-    uint2 bh[4], bl[4];           // bh[t] = {word t, word t + 4}
-};
-
-// norms are stored per problem with a stride n_pad = n rounded up to 4 (16-byte aligned
-// rows for cp.async)
-__global__ void ff_knn_prep_kernel(const int32_t *__restrict__ desc, int n, int n_pad, long long total,
-                                   KnnEntry *__restrict__ ent, long long *__restrict__ norm,
-                                   float *__restrict__ normf) {
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const long long pe = (e / n) * n_pad + e % n;
-        const int32_t *c = desc + e * 16;
-        KnnEntry k;
-        long long bn = 0;
-        unsigned *kh = reinterpret_cast<unsigned *>(k.bh), *kl = reinterpret_cast<unsigned *>(k.bl);
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const int slot = 2 * (w & 3) + (w >> 2);
-            kh[slot] = half2_bits(c[2 * w] >> 7, c[2 * w + 1] >> 7);
-            kl[slot] = half2_bits(c[2 * w] & 127, c[2 * w + 1] & 127);
-            bn += (long long)c[2 * w] * c[2 * w] + (long long)c[2 * w + 1] * c[2 * w + 1];
-        }
-        ent[e] = k;
-        norm[pe] = bn;
-        normf[pe] = float(bn);
-    }
-}
-
-__device__ __forceinline__ void cp_async16_ff(void *smem, const void *gmem) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-
-constexpr int kKnnWarps = 4;             // warps (x 16 queries) per block sharing each tile
-
-__global__ void __launch_bounds__(kKnnWarps * 32) ff_knn_mma_kernel(const KnnEntry *__restrict__ ent,
-                                                         const long long *__restrict__ norm,
-                                                         const float *__restrict__ normf, int n, int n_pad,
-                                                         int knn, int32_t *__restrict__ nn) {
-    __shared__ __align__(16) KnnEntry sE[2][kMmaTile];
-    __shared__ __align__(16) long long sN[2][kMmaTile];
-    __shared__ __align__(16) float sNf[2][kMmaTile];
-    const int prob = blockIdx.y;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const KnnEntry *eq = ent + (long long)prob * n;
-    const KnnEntry *ed = ent + (long long)(prob ^ 1) * n;
-    const long long *nq = norm + (long long)prob * n_pad, *nd = norm + (long long)(prob ^ 1) * n_pad;
-    const float *nfd = normf + (long long)(prob ^ 1) * n_pad;
-    const int q0 = (blockIdx.x * kKnnWarps + warp) * 16;
-    const int r0 = q0 + g, r1 = q0 + g + 8;
-    // A fragments (m16n8k16, row-major 16 x 16): a0 = row g, k 2t..2t+1; a1 = row g+8;
-    // a2 = row g, k 2t+8..2t+9; a3 = row g+8, k 2t+8..2t+9
-    unsigned ah[4] = {0u, 0u, 0u, 0u}, al[4] = {0u, 0u, 0u, 0u};
-    if (r0 < n) { ah[0] = eq[r0].bh[t].x; ah[2] = eq[r0].bh[t].y; al[0] = eq[r0].bl[t].x; al[2] = eq[r0].bl[t].y; }
-    if (r1 < n) { ah[1] = eq[r1].bh[t].x; ah[3] = eq[r1].bh[t].y; al[1] = eq[r1].bl[t].x; al[3] = eq[r1].bl[t].y; }
-    const long long qn0 = r0 < n ? nq[r0] : 0, qn1 = r1 < n ? nq[r1] : 0;
-    KList L0, L1;
-    klist_init(L0);
-    klist_init(L1);
-    long long thr0 = r0 < n ? 0x7fffffffffffffffll : -1ll, thr1 = r1 < n ? 0x7fffffffffffffffll : -1ll;
-    int thr0_i = 0x7fffffff, thr1_i = 0x7fffffff;
-    const float kMargin = 32768.f;
-    const float qn0f = float(qn0), qn1f = float(qn1);
-    const int ntiles = (n + kMmaTile - 1) / kMmaTile;
-    const int tq = min(int((long long)blockIdx.x * kKnnWarps * 16 / kMmaTile), ntiles - 1);
-    auto tile_of = [&](int it) {
-        const int up = ntiles - 1 - tq, dn = tq;
-        const int h = (it + 1) / 2;
-        if (it == 0) return tq;
-        if (h <= min(up, dn)) return (it & 1) ? tq + h : tq - h;
-        return up > dn ? tq + (it - dn) : tq - (it - up);
-    };
-    // cp.async one tile (64 entries x 64 B + norms) into buffer b; entries past n are not
-    // loaded (their columns are skipped by idx < n)
-    auto load_tile = [&](int it, int b) {
-        const int base = tile_of(it) * kMmaTile;
-        for (int u = threadIdx.x; u < kMmaTile * 4; u += blockDim.x) {        // 4 x 16 B per entry
-            const int e = u >> 2, part = u & 3;
-            if (base + e < n) cp_async16_ff(reinterpret_cast<char *>(&sE[b][e]) + 16 * part,
-                                            reinterpret_cast<const char *>(ed + base + e) + 16 * part);
-        }
-        for (int u = threadIdx.x; u < kMmaTile / 2; u += blockDim.x)          // norms: 2 per 16 B
-            if (base + 2 * u + 1 < n) cp_async16_ff(&sN[b][2 * u], nd + base + 2 * u);
-            else if (base + 2 * u < n) sN[b][2 * u] = nd[base + 2 * u];
-        for (int u = threadIdx.x; u < kMmaTile / 4; u += blockDim.x)          // fp32 norms: 4 per 16 B
-            if (base + 4 * u + 3 < n) cp_async16_ff(&sNf[b][4 * u], nfd + base + 4 * u);
-            else
-                for (int k = 0; k < 4; ++k)
-                    if (base + 4 * u + k < n) sNf[b][4 * u + k] = nfd[base + 4 * u + k];
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    load_tile(0, 0);
-    for (int it = 0; it < ntiles; ++it) {
-        const int b = it & 1;
-        if (it + 1 < ntiles) {
-            load_tile(it + 1, b ^ 1);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        }
-        __syncthreads();
-        const int base = tile_of(it) * kMmaTile;
-        // shared admission bound of the row: each lane sees 2 of every 8 columns; the
-        // row's final k-th best is at most the smallest of the 4 lanes' k-th best
-#pragma unroll
-        for (int m = 1; m <= 2; m <<= 1) {
-            const long long o0 = __shfl_xor_sync(0xffffffffu, thr0, m);
-            const int oi0 = __shfl_xor_sync(0xffffffffu, thr0_i, m);
-            const long long o1 = __shfl_xor_sync(0xffffffffu, thr1, m);
-            const int oi1 = __shfl_xor_sync(0xffffffffu, thr1_i, m);
-            if (o0 < thr0 || (o0 == thr0 && oi0 < thr0_i)) { thr0 = o0; thr0_i = oi0; }
-            if (o1 < thr1 || (o1 == thr1 && oi1 < thr1_i)) { thr1 = o1; thr1_i = oi1; }
-        }
-        float lim0 = float(thr0) + kMargin, lim1 = float(thr1) + kMargin;
-        // screen in the form dot >= (bn + qn - lim) / 2: per element two FFMA for the dot, one
-        // FADD and one FSETP (the row part is updated with the bound)
-        float rt0 = 0.5f * (qn0f - lim0), rt1 = 0.5f * (qn1f - lim1);
-        for (int cg = 0; cg < kMmaTile / 8; ++cg) {
-            // B fragment (16 x 8, col): b0 = k 2t..2t+1, b1 = k 2t+8..2t+9 of column g
-            const KnnEntry &E = sE[b][cg * 8 + g];
-            const uint2 bhv = E.bh[t], blv = E.bl[t];
-            const unsigned bh0 = bhv.x, bh1 = bhv.y, bl0 = blv.x, bl1 = blv.y;
-            float c1[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f}, c3[4] = {0.f, 0.f, 0.f, 0.f};
-            mma_f16(c1, ah, bh0, bh1);              // sum qh bh
-            mma_f16(c2, ah, bl0, bl1);              // + sum qh bl
-            mma_f16(c2, al, bh0, bh1);              // + sum ql bh
-            mma_f16(c3, al, bl0, bl1);              // sum ql bl
-            // fp32 screen of the 4 elements first; the exact path runs only when some lane
-            // of the warp has a survivor (rare once the lists have filled)
-            float dotf[4];
-            bool pass = false;
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-                const float bnh = 0.5f * sNf[b][cg * 8 + 2 * t + jj];
-#pragma unroll
-                for (int rr = 0; rr < 2; ++rr) {
-                    dotf[2 * rr + jj] = fmaf(16384.f, c1[2 * rr + jj], fmaf(128.f, c2[2 * rr + jj], c3[2 * rr + jj]));
-                    pass |= dotf[2 * rr + jj] >= bnh + (rr ? rt1 : rt0);
-                }
-            }
-            if (!__any_sync(0xffffffffu, pass)) continue;
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-                const int col = cg * 8 + 2 * t + jj;
-                const int idx = base + col;
-                const float bnf = sNf[b][col];
-#pragma unroll
-                for (int rr = 0; rr < 2; ++rr) {
-                    // re-test against the bound as updated by earlier insertions
-                    const float df = fmaf(-2.f, dotf[2 * rr + jj], (rr ? qn1f : qn0f) + bnf);
-                    if (df <= (rr ? lim1 : lim0) && idx < n) {
-                        const long long dot = 16384ll * (long long)c1[2 * rr + jj] +
-                                              128ll * (long long)c2[2 * rr + jj] + (long long)c3[2 * rr + jj];
-                        const long long d = (rr ? qn1 : qn0) + sN[b][col] - 2 * dot;
-                        if (rr) {
-                            KOFFER(L1, thr1, thr1_i, d, idx);
-                            lim1 = float(thr1) + kMargin;
-                            rt1 = 0.5f * (qn1f - lim1);
-                        } else {
-                            KOFFER(L0, thr0, thr0_i, d, idx);
-                            lim0 = float(thr0) + kMargin;
-                            rt0 = 0.5f * (qn0f - lim0);
-                        }
-                    }
-                }
-            }
-        }
-        __syncthreads();                             // buffer b is refilled next iteration
-    }
-    // merge the 4 partial lists of each row into lane t = 0, admitting against lane 0's own
-    // list (the shared bound may equal another lane's k-th entry, which must be merged)
-    thr0 = L0.d[knn - 1]; thr0_i = L0.i[knn - 1];
-    thr1 = L1.d[knn - 1]; thr1_i = L1.i[knn - 1];
-    for (int src = 1; src < 4; ++src) {
-        for (int k = 0; k < knn; ++k) {
-            const long long d0 = __shfl_sync(0xffffffffu, L0.d[k], (lane & ~3) | src);
-            const int i0 = __shfl_sync(0xffffffffu, L0.i[k], (lane & ~3) | src);
-            const long long d1 = __shfl_sync(0xffffffffu, L1.d[k], (lane & ~3) | src);
-            const int i1 = __shfl_sync(0xffffffffu, L1.i[k], (lane & ~3) | src);
-            if (t == 0) {
-                if (i0 != 0x7fffffff) KOFFER(L0, thr0, thr0_i, d0, i0);
-                if (i1 != 0x7fffffff) KOFFER(L1, thr1, thr1_i, d1, i1);
-            }
-        }
-    }
-    if (t == 0) {
-        if (r0 < n)
-            for (int k = 0; k < knn; ++k) nn[((long long)prob * n + r0) * knn + k] = L0.i[k];
-        if (r1 < n)
-            for (int k = 0; k < knn; ++k) nn[((long long)prob * n + r1) * knn + k] = L1.i[k];
-    }
-}
-
 // ------------------------------------------------------------------ fields
 // A field f of a batch: pair k = f / fpp, kind = f % fpp; kind 0 matches A_k -> B_k,
 // kinds 1, 2 match B_k -> A_k (the two inverse fields, F-5).
@@ -914,31 +648,17 @@ cudaError_t ff_launch_wht(const uint8_t *img, long long img_stride, int W, int H
     return cudaGetLastError();
 }
 
-size_t ff_knn_scratch_bytes(long long entries) {
-    // entries + norms with per-problem padding (<= 3 per problem; nprob <= entries)
-    return size_t(entries) * sizeof(KnnEntry) + size_t(entries) * 4 * (sizeof(long long) + sizeof(float)) + 256;
-}
+size_t ff_knn_scratch_bytes(long long entries) { return ff_knn_tc_scratch_bytes(entries); }
 
+// k nearest descriptors of every entry of problem p (query image p) in image p ^ 1: windows
+// up to 8x8 on the tensor cores (knn_tc.cu: coefficients < 2^14 split into exact limbs), the
+// 16x16 window (coefficients up to 2^16) on the fp64 CUDA-core kernel
 cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int win, int32_t *nn, void *scratch,
                           cudaStream_t st) {
     if (knn < 1 || knn > kKnnMax) return cudaErrorInvalidValue;
-    static const bool legacy = getenv("SGM_KNN_MMA_SYNC") != nullptr;   // A/B experiments only
-    if (win <= 8 && !legacy) return ff_launch_knn_tc(desc, n, nprob, knn, nn, scratch, st);
-    if (win <= 8) {                         // coefficients fit two exact limbs: tensor cores
-        // every problem's query image and its partner database image (nprob may be odd: one
-        // problem of a pair)
-        const long long total = (long long)n * (nprob + (nprob & 1));
-        const int n_pad = (n + 3) & ~3;
-        KnnEntry *ent = reinterpret_cast<KnnEntry *>(scratch);
-        long long *norm = reinterpret_cast<long long *>(ent + total);
-        float *normf = reinterpret_cast<float *>(norm + (long long)n_pad * (nprob + (nprob & 1)));
-        ff_knn_prep_kernel<<<ff_grid(total, 128), 128, 0, st>>>(desc, n, n_pad, total, ent, norm, normf);
-        dim3 grid((n + kKnnWarps * 16 - 1) / (kKnnWarps * 16), nprob);
-        ff_knn_mma_kernel<<<grid, kKnnWarps * 32, 0, st>>>(ent, norm, normf, n, n_pad, knn, nn);
-    } else {
-        dim3 grid((n + 127) / 128, nprob);
-        ff_knn_kernel<<<grid, 128, 0, st>>>(desc, n, knn, nn);
-    }
+    if (win <= 8) return ff_launch_knn_tc(desc, n, nprob, knn, nn, scratch, st);
+    dim3 grid((n + 127) / 128, nprob);
+    ff_knn_kernel<<<grid, 128, 0, st>>>(desc, n, knn, nn);
     return cudaGetLastError();
 }
 

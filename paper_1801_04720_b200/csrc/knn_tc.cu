@@ -3,61 +3,74 @@
 // reading FF5: the exact k nearest by squared Euclidean distance, ties to the smaller
 // database index -- the result of an exact k-d tree query).
 //
-// Exactness.  Each 16-coefficient descriptor c (|c| < 2^14, 8x8 WHT window) splits into two
-// fp16 limbs c = 128 h + l, |h| <= 128, 0 <= l <= 127, both exact in fp16, so
-//   q . b = 16384 sum(qh bh) + 128 sum(qh bl + ql bh) + sum(ql bl)
-// where every product is < 2^14 and every 16- or 32-term sum < 2^24: the fp32 tensor-core
-// accumulators hold the three sums exactly.  The epilogue screens each (query, entry)
-// distance |q|^2 + |b|^2 - 2 q.b in fp32 against the query's admission bound plus a 2^15
-// margin (fp32 error < 2^13) and forms the exact 64-bit distance only for survivors.
+// Exact integer dot products on the tensor cores.  Each 16-coefficient descriptor c
+// (|c| < 2^14, 8x8 WHT window) splits into limbs c = 128 h + l, |h| <= 128, 0 <= l <= 127,
+// and its norm |b|^2 < 2^32 into four bytes n3..n0; all of them and the scale factors used
+// below are exact bf16 values.  Seven K=16 MMAs (bf16 in, fp32 accumulate) fill three
+// accumulators per (query, entry):
+//   A1 = 16384 qh.bh - 2^23 n3 - 2^15 n2          (multiples of 2^14, |A1| < 2^33)
+//   A2 = 128 qh.bl + 128 ql.bh - 128 n1            (multiples of 2^7,  |A2| < 2^27)
+//   A3 = ql.bl - n0 / 2                            (multiples of 1/2,  |A3| < 2^18)
+// Every partial sum of each stays on its grid within 2^24 steps, so all three are EXACT in
+// fp32, and A1 + A2 + A3 = q.b - |b|^2 / 2 =: D, i.e. |q - b|^2 = |q|^2 - 2 D.  The screen
+// forms D in fp32 (two additions, error <= 2^10) and admits a candidate when D >= (|q|^2 -
+// bound) / 2 - 2^11; the exact path re-adds A1, A2, A3 in 64-bit integers (2 A_k are
+// integers), so the (distance, index)-ordered top-k is exactly the oracle's.
 //
-// Blackwell mapping (sm_100a): one CTA = 128 queries = the 128 TMEM lanes; per database
-// tile of 64 entries one elected thread issues four tcgen05.mma.kind::f16 (M=128, N=64,
-// K=16; A = query limbs, B = entry limbs, both K-major in shared memory, no swizzle) into
-// three fp32 accumulators in TMEM (sum hh, sum hl + lh, sum ll: 192 columns), commits them
-// to an mbarrier, and every thread reads ITS query row back with tcgen05.ld (32x32b: warp
-// w owns lanes 32w..32w+31) -- so a thread screens 64 candidates of one row with no
-// fragment shuffling, and keeps that row's (distance, index) top-k alone.  Database tiles
-// are staged by cp.async in a 3-stage ring; tiles are visited nearest-first (the query
-// block's own position outward: descriptors of nearby pixels are similar, so the bounds
-// tighten early and the exact path stays rare).
-#include <cuda_fp16.h>
+// Blackwell mapping (sm_100a): one CTA = 128 queries = the 128 TMEM lanes; database tiles of
+// 32 entries (B operand [bh | bl | n3 n2 n1 n0 0..], K-major, no swizzle) are staged by
+// cp.async in a 4-deep ring; one elected thread issues the seven tcgen05.mma.kind::f16 of
+// tile t+1 (M=128, N=32) into the other of two TMEM buffers (3 accumulators x 32 columns
+// each) while every thread screens tile t from TMEM (tcgen05.ld 32x32b: warp w owns lanes
+// 32w..32w+31, so a thread reads ITS query's candidates and keeps its top-k alone): per
+// candidate two FADD and one FMNMX (the chunk maximum against the bound); the per-candidate
+// test runs only in chunks that pass.  256 TMEM columns per CTA: 2 CTAs share an SM.  Tiles
+// are visited nearest-first (the query block's own position outward): descriptors of nearby
+// pixels are similar, so the bounds tighten early and the exact path stays rare.
+#include <cuda_bf16.h>
 
 #include "sgm_internal.cuh"
 
 namespace sgm {
 namespace {
 
-constexpr int kTcM = 128;          // queries per CTA (TMEM lanes, MMA M)
-constexpr int kTcN = 64;           // database entries per tile (MMA N)
-constexpr int kTcStages = 3;       // database tiles in flight
+constexpr int kTcM = 128;              // queries per CTA (TMEM lanes, MMA M)
+constexpr int kTcN = 32;               // database entries per tile (MMA N)
+constexpr int kTcStages = 8;           // database tiles in flight (TMA bulk-copy ring)
 constexpr int kTcKnnMax = 8;
-constexpr uint32_t kTmemCols = 256;   // >= 3 accumulators x kTcN columns, power of two
+constexpr uint32_t kTmemCols = 256;    // 2 buffers x 3 accumulators x kTcN columns (2 CTAs/SM)
+constexpr int kAK = 112;               // A row: 7 K-blocks of 16 bf16
+constexpr int kBK = 48;                // B row: bh, bl, norm bytes (3 K-blocks)
+constexpr float kMarginHalf = 2048.f;  // screen slack on D (fp32 error of A1 + A2 + A3 <= 2^10)
 
-// Prepared entry: 16 hi limbs then 16 lo limbs, fp16, natural coefficient order (64 B).
+// Prepared database entry (96 B): 16 hi limbs, 16 lo limbs, the 4 bytes of |b|^2 (high
+// first) then 12 zeros, all bf16.  The prep kernel stores them tile by tile (kTcN entries)
+// already in the canonical B layout, so one TMA bulk copy moves a whole tile.
 struct TcEntry {
-    __half h[16];
-    __half l[16];
+    __nv_bfloat16 h[16], l[16], nb[16];
 };
+constexpr int kTileBytes = kTcN * kBK * 2;       // 3 KB per database tile
 
 // canonical K-major, no-swizzle operand layout (UMMA "interleave"): 8-row x 16-byte core
-// matrices, the two 8-element K halves of a row 128 B apart (LBO), 8-row groups 256 B
-// apart (SBO): row r, K half c at byte (r / 8) * 256 + c * 128 + (r % 8) * 16
-__device__ __forceinline__ uint32_t canon_off(int r, int c) { return (r >> 3) * 256 + c * 128 + (r & 7) * 16; }
+// matrices; the 16-byte K chunks of a row 128 B apart (LBO), 8-row groups `sbo` bytes apart
+__device__ __forceinline__ uint32_t canon_off(int r, int chunk, int sbo) {
+    return (r >> 3) * sbo + chunk * 128 + (r & 7) * 16;
+}
 
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t sbo) {
     uint64_t d = 0;
     d |= uint64_t((saddr >> 4) & 0x3FFF);            // start address
-    d |= uint64_t(128 >> 4) << 16;                   // LBO: K-half to K-half
-    d |= uint64_t(256 >> 4) << 32;                   // SBO: 8-row group to 8-row group
+    d |= uint64_t(128 >> 4) << 16;                   // LBO: K chunk to K chunk
+    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;        // SBO: 8-row group to 8-row group
     d |= uint64_t(1) << 46;                          // descriptor version (sm_100)
     return d;                                        // base offset 0, no swizzle
 }
 
-// kind::f16 instruction descriptor: fp32 accumulator, fp16 A and B, both K-major, N, M
-constexpr uint32_t kIdesc = (1u << 4) | (uint32_t(kTcN >> 3) << 17) | (uint32_t(kTcM >> 4) << 24);
+// kind::f16 instruction descriptor: fp32 accumulator, bf16 A and B, both K-major, N, M
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kTcN >> 3) << 17) |
+                            (uint32_t(kTcM >> 4) << 24);
 
-__device__ __forceinline__ void mma_f16_tc(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t accumulate) {
+__device__ __forceinline__ void mma_bf16(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t accumulate) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
         " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
@@ -68,32 +81,42 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+    for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
 }
 
-__device__ __forceinline__ void cp16(uint32_t saddr, const void *g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g) : "memory");
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t par) {
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(par)
+        : "memory");
 }
 
 // (distance, index)-ordered top-k of one query row (insertions are rare once it has filled)
+// (distances are integers below 2^34: exact in fp64)
 struct TcList {
-    long long d[kTcKnnMax];
+    double d[kTcKnnMax];
     int i[kTcKnnMax];
 };
 
-__device__ __noinline__ void tclist_insert(TcList *L, long long dv, int ci, int knn) {
+__device__ __noinline__ void tclist_insert(TcList *L, double dv, int ci, int knn) {
     bool ins = false;
     for (int k = 0; k < knn; ++k) {
         if (ins || dv < L->d[k] || (dv == L->d[k] && ci < L->i[k])) {
-            const long long td = L->d[k];
+            const double td = L->d[k];
             const int ti = L->i[k];
             L->d[k] = dv; L->i[k] = ci; dv = td; ci = ti;
             ins = true;
@@ -101,76 +124,68 @@ __device__ __noinline__ void tclist_insert(TcList *L, long long dv, int ci, int 
     }
 }
 
-__global__ void ff_knn_tc_prep_kernel(const int32_t *__restrict__ desc, int n, int n_pad, long long total,
-                                      TcEntry *__restrict__ ent, long long *__restrict__ norm,
-                                      float *__restrict__ normf) {
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+// entries of problem p (query image p) in tiles: tile t holds entries kTcN t .. kTcN t + kTcN-1
+// (zero past n) in the canonical B layout (row = entry, 16-byte chunks 0-1 hi limbs, 2-3 lo
+// limbs, 4-5 norm bytes)
+__global__ void ff_knn_tc_prep_kernel(const int32_t *__restrict__ desc, int n, int ntiles, long long total_pad,
+                                      unsigned char *__restrict__ tiles) {
+    constexpr uint32_t kSboB = (kBK / 8) * 128;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total_pad;
          e += (long long)gridDim.x * blockDim.x) {
-        const long long pe = (e / n) * n_pad + e % n;
-        const int32_t *c = desc + e * 16;
+        const long long per = (long long)ntiles * kTcN;
+        const long long prob = e / per;
+        const int i = int(e - prob * per);                 // entry index within the problem
         TcEntry t;
-        long long bn = 0;
+        unsigned long long bn = 0;
+        if (i < n) {
+            const int32_t *c = desc + (prob * n + i) * 16;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            t.h[k] = __int2half_rn(c[k] >> 7);       // floor division: c = 128 h + l
-            t.l[k] = __int2half_rn(c[k] & 127);
-            bn += (long long)c[k] * c[k];
+            for (int k = 0; k < 16; ++k) {
+                t.h[k] = __int2bfloat16_rn(c[k] >> 7);    // floor division: c = 128 h + l
+                t.l[k] = __int2bfloat16_rn(c[k] & 127);
+                bn += (unsigned long long)((long long)c[k] * c[k]);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) t.h[k] = t.l[k] = __int2bfloat16_rn(0);
         }
-        ent[e] = t;
-        norm[pe] = bn;
-        normf[pe] = float(bn);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) t.nb[k] = __int2bfloat16_rn(k < 4 ? int((bn >> (8 * (3 - k))) & 255u) : 0);
+        unsigned char *tile = tiles + (prob * ntiles + i / kTcN) * (long long)kTileBytes;
+        const uint4 *src = reinterpret_cast<const uint4 *>(&t);
+#pragma unroll
+        for (int ch = 0; ch < kBK / 8; ++ch) *reinterpret_cast<uint4 *>(tile + canon_off(i % kTcN, ch, kSboB)) = src[ch];
     }
 }
 
 struct __align__(128) TcSmem {
-    unsigned char qh[kTcM * 32], ql[kTcM * 32];                    // A operands (canonical)
-    unsigned char bh[kTcStages][kTcN * 32], bl[kTcStages][kTcN * 32];   // B operands
-    long long bn[kTcStages][kTcN];
-    float bnf[kTcStages][kTcN];
-    uint64_t mma_bar;
+    unsigned char a[kTcM * kAK * 2];                            // A operand (canonical)
+    unsigned char b[kTcStages][kTileBytes];                     // B operand ring
+    uint64_t loaded[kTcStages];                                 // TMA -> MMA (B stage)
+    uint64_t full[2];                                           // MMA -> epilogue (TMEM buffer)
+    uint64_t empty[2];                                          // epilogue -> MMA (TMEM buffer)
     uint32_t tmem_base;
 };
 
-__global__ void __launch_bounds__(kTcM) ff_knn_tc_kernel(const TcEntry *__restrict__ ent,
-                                                         const long long *__restrict__ norm,
-                                                         const float *__restrict__ normf, int n, int n_pad,
-                                                         int knn, int32_t *__restrict__ nn) {
+constexpr int kTcEpiWarps = kTcM / 32;          // 4 epilogue warps (one query row per thread)
+constexpr int kTcThreads = kTcM + 32;           // + 1 producer warp (TMA + MMA issue)
+
+__device__ __forceinline__ void mbar_arrive_cta(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads) ff_knn_tc_kernel(const unsigned char *__restrict__ tiles, int n,
+                                                               int knn, int32_t *__restrict__ nn) {
     extern __shared__ unsigned char smem_raw[];
     TcSmem &S = *reinterpret_cast<TcSmem *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    constexpr uint32_t kSboA = (kAK / 8) * 128, kSboB = (kBK / 8) * 128;
     const int prob = blockIdx.y;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const TcEntry *eq = ent + (long long)prob * n;
-    const TcEntry *ed = ent + (long long)(prob ^ 1) * n;
-    const long long *nd = norm + (long long)(prob ^ 1) * n_pad;
-    const float *nfd = normf + (long long)(prob ^ 1) * n_pad;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int q0 = blockIdx.x * kTcM;
-    const int row = q0 + tid;                        // this thread's query (TMEM lane tid)
-
-    if (warp == 0) {                                 // TMEM for the three accumulators
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&S.tmem_base)),
-                     "n"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&S.mma_bar)));
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    // this thread's query limbs into the A operands (rows past n stay zero)
-    {
-        uint4 h0 = make_uint4(0, 0, 0, 0), h1 = h0, l0 = h0, l1 = h0;
-        if (row < n) {
-            const uint4 *src = reinterpret_cast<const uint4 *>(eq + row);
-            h0 = src[0]; h1 = src[1]; l0 = src[2]; l1 = src[3];
-        }
-        *reinterpret_cast<uint4 *>(S.qh + canon_off(tid, 0)) = h0;
-        *reinterpret_cast<uint4 *>(S.qh + canon_off(tid, 1)) = h1;
-        *reinterpret_cast<uint4 *>(S.ql + canon_off(tid, 0)) = l0;
-        *reinterpret_cast<uint4 *>(S.ql + canon_off(tid, 1)) = l1;
-    }
-    const long long qn = row < n ? norm[(long long)prob * n_pad + row] : 0;
-    const float qnf = float(qn);
-
+    const int row = q0 + tid;                        // epilogue threads: this query (TMEM lane tid)
     const int ntiles = (n + kTcN - 1) / kTcN;
+    const unsigned char *tq_base = tiles + (long long)prob * ntiles * kTileBytes;          // queries
+    const unsigned char *td_base = tiles + (long long)(prob ^ 1) * ntiles * kTileBytes;    // database
     const int tq = min(q0 / kTcN, ntiles - 1);
     auto tile_of = [&](int it) {                     // nearest-first visiting order
         const int up = ntiles - 1 - tq, dn = tq;
@@ -179,139 +194,207 @@ __global__ void __launch_bounds__(kTcM) ff_knn_tc_kernel(const TcEntry *__restri
         if (h <= min(up, dn)) return (it & 1) ? tq + h : tq - h;
         return up > dn ? tq + (it - dn) : tq - (it - up);
     };
-    // cp.async one database tile (limbs in the canonical B layout + norms) into stage s;
-    // entries past n are zero-filled (their distances are masked by idx < n)
-    auto load_tile = [&](int it, int s) {
-        if (it < ntiles) {
-            const int base = tile_of(it) * kTcN;
-            for (int u = tid; u < kTcN * 4; u += kTcM) {          // 4 x 16 B per entry
-                const int e = u >> 2, part = u & 3;                // part: h0 h1 l0 l1
-                unsigned char *dst = (part < 2 ? S.bh[s] : S.bl[s]) + canon_off(e, part & 1);
-                if (base + e < n) cp16(smem_u32(dst), reinterpret_cast<const char *>(ed + base + e) + 16 * part);
-                else *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
-            }
-            for (int e = tid; e < kTcN; e += kTcM) {
-                if (base + e < n) {
-                    S.bn[s][e] = nd[base + e];
-                    S.bnf[s][e] = nfd[base + e];
-                } else {
-                    S.bn[s][e] = 0;
-                    S.bnf[s][e] = 3.0e38f;                         // never passes the screen
-                }
-            }
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    for (int s = 0; s < kTcStages - 1; ++s) load_tile(s, s);
 
+    if (warp == 0) {                                 // TMEM: two buffers of 3 accumulators
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&S.tmem_base)),
+                     "n"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        for (int k = 0; k < kTcStages; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&S.loaded[k])));
+        for (int k = 0; k < 2; ++k) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&S.full[k])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&S.empty[k])), "r"(kTcEpiWarps));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    // epilogue threads: the A row of their query, K-blocks 0: 16384 qh, 1: 128 qh, 2: 128 ql,
+    // 3: ql, 4: (-2^23, -2^15, 0..), 5: (0, 0, -2^7, 0..), 6: (0, 0, 0, -1/2, 0..); rows past
+    // n stay zero
+    long long qn = 0;
+    if (warp < kTcEpiWarps) {
+        __nv_bfloat16 av[kAK];
+#pragma unroll
+        for (int k = 0; k < kAK; ++k) av[k] = __float2bfloat16_rn(0.f);
+        if (row < n) {
+            const unsigned char *qt = tq_base + (long long)(row / kTcN) * kTileBytes;
+            TcEntry e;
+            uint4 *ev = reinterpret_cast<uint4 *>(&e);
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) ev[ch] = *reinterpret_cast<const uint4 *>(qt + canon_off(row % kTcN, ch, kSboB));
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const float h = __bfloat162float(e.h[k]), l = __bfloat162float(e.l[k]);
+                av[k] = __float2bfloat16_rn(16384.f * h);
+                av[16 + k] = __float2bfloat16_rn(128.f * h);
+                av[32 + k] = __float2bfloat16_rn(128.f * l);
+                av[48 + k] = e.l[k];
+                const long long qk = 128 * (long long)h + (long long)l;
+                qn += qk * qk;
+            }
+            av[64] = __float2bfloat16_rn(-8388608.f);
+            av[65] = __float2bfloat16_rn(-32768.f);
+            av[80 + 2] = __float2bfloat16_rn(-128.f);
+            av[96 + 3] = __float2bfloat16_rn(-0.5f);
+        }
+        const uint4 *src = reinterpret_cast<const uint4 *>(av);
+#pragma unroll
+        for (int ch = 0; ch < kAK / 8; ++ch) *reinterpret_cast<uint4 *>(S.a + canon_off(tid, ch, kSboA)) = src[ch];
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // A is read by the MMA
+    }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = S.tmem_base;
-    const uint32_t t_c1 = tmem, t_c2 = tmem + kTcN, t_c3 = tmem + 2 * kTcN;
-    const uint32_t lane_off = uint32_t(warp * 32) << 16;          // this warp's TMEM lanes
-    const uint64_t dqh = smem_desc(smem_u32(S.qh)), dql = smem_desc(smem_u32(S.ql));
 
-    TcList L;
-    for (int k = 0; k < kTcKnnMax; ++k) { L.d[k] = 0x7fffffffffffffffll; L.i[k] = 0x7fffffff; }
-    long long thr = row < n ? 0x7fffffffffffffffll : -1ll;        // admission bound (k-th)
-    int thr_i = 0x7fffffff;
-    const float kMargin = 32768.f;
-    float rt = 0.5f * (qnf - (float(thr) + kMargin));             // screen: dot >= bn/2 + rt
-
-    for (int it = 0; it < ntiles; ++it) {
-        const int s = it % kTcStages;
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcStages - 2) : "memory");
-        // the tile's shared-memory bytes (cp.async / st.shared: generic proxy) must be visible
-        // to the tensor core (async proxy); the previous tile's TMEM reads must be complete
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        if (tid == 0) {
-            const uint64_t dbh = smem_desc(smem_u32(S.bh[s])), dbl = smem_desc(smem_u32(S.bl[s]));
-            mma_f16_tc(t_c1, dqh, dbh, 0);           // sum qh bh
-            mma_f16_tc(t_c2, dqh, dbl, 0);           // sum qh bl
-            mma_f16_tc(t_c2, dql, dbh, 1);           //   + sum ql bh
-            mma_f16_tc(t_c3, dql, dbl, 0);           // sum ql bl
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                             smem_u32(&S.mma_bar))
-                         : "memory");
-        }
-        load_tile(it + kTcStages - 1, (it + kTcStages - 1) % kTcStages);   // that stage is free
-        {
-            const uint32_t bar = smem_u32(&S.mma_bar), par = uint32_t(it & 1);
-            asm volatile(
-                "{\n .reg .pred P1;\n"
-                "WAIT_%=:\n"
-                " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-                " @!P1 bra WAIT_%=;\n}\n" ::"r"(bar),
-                "r"(par)
-                : "memory");
-        }
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const int base = tile_of(it) * kTcN;
-#pragma unroll 1
-        for (int ch = 0; ch < kTcN / 16; ++ch) {
-            float c1[16], c2[16], c3[16];
-            __syncwarp();                            // tcgen05.ld is warp-collective
-            tmem_ld16(t_c1 + lane_off + 16 * ch, c1);
-            tmem_ld16(t_c2 + lane_off + 16 * ch, c2);
-            tmem_ld16(t_c3 + lane_off + 16 * ch, c3);
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-            unsigned pass = 0;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const float dot = fmaf(16384.f, c1[j], fmaf(128.f, c2[j], c3[j]));
-                pass |= (dot >= fmaf(0.5f, S.bnf[s][16 * ch + j], rt) ? 1u : 0u) << j;
+    if (warp == kTcEpiWarps) {
+        // ---------------- producer warp: database tiles (TMA ring) and the MMAs
+        auto load_tile = [&](int it) {               // one bulk copy per tile, on loaded[stage]
+            if (it < ntiles && lane == 0) {
+                const int st = it % kTcStages;
+                const uint32_t bar = smem_u32(&S.loaded[st]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "n"(kTileBytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                        smem_u32(S.b[st])),
+                    "l"(td_base + (long long)tile_of(it) * kTileBytes), "n"(kTileBytes), "r"(bar)
+                    : "memory");
             }
-            while (pass) {                           // exact path (rare once the list has filled)
-                const int j = __ffs(pass) - 1;
-                pass &= pass - 1;
-                const int col = 16 * ch + j;
-                const long long dot = 16384ll * (long long)c1[j] + 128ll * (long long)c2[j] + (long long)c3[j];
-                const long long d = qn + S.bn[s][col] - 2 * dot;
-                const int idx = base + col;
-                if (d < thr || (d == thr && idx < thr_i)) {
-                    tclist_insert(&L, d, idx, knn);
-                    thr = L.d[knn - 1];
-                    thr_i = L.i[knn - 1];
-                    rt = 0.5f * (qnf - (float(thr) + kMargin));
+        };
+        for (int s0 = 0; s0 < kTcStages; ++s0) load_tile(s0);
+        // the seven MMAs (the three accumulators interleaved: dependent MMAs apart):
+        // A K-block, B K-block (0 bh, 1 bl, 2 norm bytes), accumulator, accumulate
+        constexpr int ablk[7] = {0, 1, 3, 4, 2, 6, 5};
+        constexpr int bblk[7] = {0, 1, 1, 2, 0, 2, 2};
+        constexpr int acc[7] = {0, 1, 2, 0, 1, 2, 1};
+        constexpr int add[7] = {0, 0, 0, 1, 1, 1, 1};
+        const uint32_t a_base = smem_u32(S.a);
+        uint64_t adesc[7];
+#pragma unroll
+        for (int i = 0; i < 7; ++i) adesc[i] = smem_desc(a_base + 2 * ablk[i] * 128, kSboA);
+        const uint64_t bdesc0 = smem_desc(smem_u32(S.b[0]), kSboB);
+        for (int it = 0; it < ntiles; ++it) {
+            if (it >= 2) {
+                // TMEM buffer it & 1 drained by the epilogue (tile it-2), which also means tile
+                // it-2's MMAs completed: its stage takes tile it-2+S (the producer never waits
+                // for the MMA it just issued, so the tensor core always has the next tile)
+                mbar_wait_parity(smem_u32(&S.empty[it & 1]), uint32_t(((it - 2) >> 1) & 1));
+                load_tile(it - 2 + kTcStages);
+            }
+            mbar_wait_parity(smem_u32(&S.loaded[it % kTcStages]), uint32_t((it / kTcStages) & 1));
+            __syncwarp();
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (lane == 0) {
+                const uint64_t bd = bdesc0 + uint64_t(((it % kTcStages) * kTileBytes) >> 4);
+                const uint32_t d = tmem + uint32_t((it & 1) * 3 * kTcN);
+#pragma unroll
+                for (int i = 0; i < 7; ++i)
+                    mma_bf16(d + uint32_t(acc[i] * kTcN), adesc[i], bd + uint64_t((2 * bblk[i] * 128) >> 4),
+                             uint32_t(add[i]));
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                 smem_u32(&S.full[it & 1]))
+                             : "memory");
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---------------- epilogue warps: screen every candidate of this query, exact path
+        TcList L;
+        for (int k = 0; k < kTcKnnMax; ++k) { L.d[k] = 1e308; L.i[k] = 0x7fffffff; }
+        double thr = row < n ? 1e308 : -1.0;                          // admission bound (k-th)
+        int thr_i = 0x7fffffff;
+        const double qnd = double(qn);                                // exact (< 2^33)
+        const float qnh = 0.5f * float(qn);
+        // screen: D >= rt, rt = (|q|^2 - bound) / 2 - slack; -inf until the list has filled
+        float rt = row < n ? -3.0e38f : 3.0e38f;
+        const uint32_t lane_off = uint32_t(warp * 32) << 16;          // this warp's TMEM lanes
+        for (int it = 0; it < ntiles; ++it) {
+            mbar_wait_parity(smem_u32(&S.full[it & 1]), uint32_t((it >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            float A1[32], A2[32], A3[32];
+            const uint32_t tb = tmem + lane_off + uint32_t((it & 1) * 3 * kTcN);
+            __syncwarp();                            // tcgen05.ld is warp-collective
+            tmem_ld32(tb, A1);
+            tmem_ld32(tb + kTcN, A2);
+            tmem_ld32(tb + 2 * kTcN, A3);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta(smem_u32(&S.empty[it & 1]));   // buffer drained
+            const int base = tile_of(it) * kTcN;
+            // D = A1 + A2 + A3 (fp32); the maximum per group of 8 candidates against the bound,
+            // the per-candidate test only inside groups that pass (a candidate that enters is
+            // rare per query, but 32 queries share a warp)
+            float D[32], gm[4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+#pragma unroll
+                for (int j = 8 * g; j < 8 * g + 8; ++j) D[j] = (A1[j] + A2[j]) + A3[j];
+                gm[g] = fmaxf(fmaxf(fmaxf(D[8 * g], D[8 * g + 1]), fmaxf(D[8 * g + 2], D[8 * g + 3])),
+                              fmaxf(fmaxf(D[8 * g + 4], D[8 * g + 5]), fmaxf(D[8 * g + 6], D[8 * g + 7])));
+            }
+            if (fmaxf(fmaxf(gm[0], gm[1]), fmaxf(gm[2], gm[3])) >= rt) {
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    if (!(gm[g] >= rt)) continue;
+#pragma unroll
+                    for (int j = 8 * g; j < 8 * g + 8; ++j) {
+                        if (!(D[j] >= rt)) continue;
+                        const int idx = base + j;
+                        if (idx >= n) continue;
+                        // exact in fp64: A1, A2, A3 are exact fp32 values, their sum (< 2^34,
+                        // a multiple of 1/2) is exact in fp64: d = |q|^2 - 2 D
+                        const double dd = qnd - 2.0 * ((double(A1[j]) + double(A2[j])) + double(A3[j]));
+                        if (dd < thr || (dd == thr && idx < thr_i)) {
+                            tclist_insert(&L, dd, idx, knn);
+                            thr = L.d[knn - 1];
+                            thr_i = L.i[knn - 1];
+                            if (thr < 1e300) rt = qnh - 0.5f * float(thr) - kMarginHalf;
+                        }
+                    }
                 }
             }
         }
+        if (row < n)
+            for (int k = 0; k < knn; ++k) nn[((long long)prob * n + row) * knn + k] = L.i[k];
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols));
-    if (row < n)
-        for (int k = 0; k < knn; ++k) nn[((long long)prob * n + row) * knn + k] = L.i[k];
 }
 
 }  // namespace
 
-size_t ff_knn_tc_smem() { return sizeof(TcSmem) + 128; }
+size_t ff_knn_tc_scratch_bytes(long long entries) {
+    // nprob <= entries problems, each padded by < kTcN entries
+    return size_t(2 * entries + kTcN) * sizeof(TcEntry) + 256;
+}
 
 // tensor-core kNN of nprob problems (query image p, database image p ^ 1) over n entries
 cudaError_t ff_launch_knn_tc(const int32_t *desc, int n, int nprob, int knn, int32_t *nn, void *scratch,
                              cudaStream_t st) {
     if (knn < 1 || knn > kTcKnnMax) return cudaErrorInvalidValue;
-    const long long total = (long long)n * (nprob + (nprob & 1));
-    const int n_pad = (n + 3) & ~3;
-    TcEntry *ent = reinterpret_cast<TcEntry *>(scratch);
-    long long *norm = reinterpret_cast<long long *>(ent + total);
-    float *normf = reinterpret_cast<float *>(norm + (long long)n_pad * (nprob + (nprob & 1)));
-    long long g = (total + 127) / 128;
+    const int np = nprob + (nprob & 1);
+    const int ntiles = (n + kTcN - 1) / kTcN;
+    const long long total_pad = (long long)np * ntiles * kTcN;
+    unsigned char *tiles = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(scratch) + 127) & ~uintptr_t(127));
+    long long g = (total_pad + 127) / 128;
     if (g > 148LL * 16) g = 148LL * 16;
-    ff_knn_tc_prep_kernel<<<unsigned(g < 1 ? 1 : g), 128, 0, st>>>(desc, n, n_pad, total, ent, norm, normf);
+    ff_knn_tc_prep_kernel<<<unsigned(g < 1 ? 1 : g), 128, 0, st>>>(desc, n, ntiles, total_pad, tiles);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const size_t sm = ff_knn_tc_smem();
+    // the TMEM of an SM holds 512 / kTmemCols = 2 CTAs: request enough shared memory that no
+    // third CTA becomes resident (it would spin in tcgen05.alloc)
+    size_t sm = sizeof(TcSmem) + 128;
+    if (sm < 80 * 1024) sm = 80 * 1024;
     if ((e = cudaFuncSetAttribute(ff_knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))) != cudaSuccess)
         return e;
     dim3 grid((n + kTcM - 1) / kTcM, nprob);
-    ff_knn_tc_kernel<<<grid, kTcM, sm, st>>>(ent, norm, normf, n, n_pad, knn, nn);
+    ff_knn_tc_kernel<<<grid, kTcThreads, sm, st>>>(tiles, n, knn, nn);
     return cudaGetLastError();
 }
 

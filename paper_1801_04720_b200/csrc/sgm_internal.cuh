@@ -162,6 +162,7 @@ cudaError_t ff_launch_wht(const uint8_t *img, long long img_stride, int W, int H
 cudaError_t ff_launch_knn(const int32_t *desc, int n, int nprob, int knn, int win, int32_t *nn, void *scratch,
                           cudaStream_t st);
 size_t ff_knn_scratch_bytes(long long entries);
+size_t ff_knn_tc_scratch_bytes(long long entries);
 cudaError_t ff_launch_knn_tc(const int32_t *desc, int n, int nprob, int knn, int32_t *nn, void *scratch,
                              cudaStream_t st);
 cudaError_t ff_launch_init(const FFFields &F, const int32_t *nn, int knn, cudaStream_t st);

@@ -20,8 +20,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__grid_size"]
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-        "msecond": 1e-3}
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1e-9,
+        "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
 
 
 def raw(rep):
@@ -58,7 +58,10 @@ def main(reps):
             d = dict(zip(hdr, row))
             u = dict(zip(hdr, units))
             name = d["Kernel Name"]
-            bwd = "(bool)1, (bool)1," in name.replace(" ", " ") or re.search(r"sweep_kernel<\(int\)\d+, \(bool\)\d, \(bool\)1", name)
+            # template arguments: <CPL, C64, BWD, ...> (sweep_kernel / stair_kernel)
+            targs = re.search(r"_kernel<([^>]*)>", name).group(1).replace("(int)", "").replace("(bool)", "")
+            targs = [a.strip() for a in targs.split(",")]
+            bwd = targs[2] in ("1", "true")
             kern = "sweep_bwd_wta" if bwd else "sweep_fwd"
 
             def val(k):
