@@ -165,14 +165,16 @@ def measured_peaks():
 
 def ncu_traffic(config, kernel, quads):
     """DRAM bytes (read + write) per launch of `kernel` scaled to `quads` quads, from the
-    committed `ncu --set full` capture (profiles/ncu_traffic.json: {"<config>/<kernel>":
-    {"bytes": per launch, "quads": quads of that launch}}), else None."""
+    committed `ncu --set full` capture (profiles/ncu_traffic.json: {"<config>x<quads>/<kernel>"
+    or "<config>/<kernel>": {"bytes": per launch, "quads": quads of that launch}}; the capture
+    of the same quad count first), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            rec = json.load(f).get(f"{config}/{kernel}")
+            table = json.load(f)
     except (OSError, ValueError):
         return None
+    rec = table.get(f"{config}x{quads}/{kernel}") or table.get(f"{config}/{kernel}")
     if not isinstance(rec, dict) or not rec.get("quads"):
         return None
     return rec["bytes"] * quads / rec["quads"]
@@ -428,8 +430,8 @@ class Runner:
         self.sgm.close()
 
 
-def config_entry(cfg, n, runner, steps, peaks, peak_src):
-    ms = runner.timed(runner.run_once, steps)
+def config_entry(cfg, n, runner, steps, warmup, peaks, peak_src):
+    ms = runner.timed(runner.run_once, steps, warmup=max(warmup, 3))
     st, lps = runner.stage_times(max(3, min(steps, 10)))
     m = statistics.mean(ms)
     return {"quads": n, "W": cfg.W, "H": cfg.H, "D": cfg.D,
@@ -591,7 +593,7 @@ def main():
                 continue
             qs = synth.make_batch(c, 0, n, workers=max(1, min(n, cores)))
             r = Runner(c, qs, dev, graph=not args.no_graph)
-            configs[f"{name}x{n}"] = config_entry(c, n, r, args.steps, peaks, peak_src)
+            configs[f"{name}x{n}"] = config_entry(c, n, r, args.steps, args.warmup, peaks, peak_src)
             r.close()
             del r, qs
             torch.cuda.empty_cache()

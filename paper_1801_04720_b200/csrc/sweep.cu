@@ -130,8 +130,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     const int wid = int(__reduce_min_sync(0xffffffffu, threadIdx.x >> 5));
     // row of the band this warp computes: the band's first (upstream) row runs on the
     // highest compute-warp id (the warp arbiter favours high warp ids, so upstream rows win
-    // ties and downstream rows find their inputs ready: 6.77 -> 6.73 ms on 8 Driving quads)
-    const int warp = wid == NW ? wid : NW - 1 - wid;
+    // ties and downstream rows find their inputs ready: 6.79 -> 6.67 ms on 8 Driving quads).
+    // For 8 cells per lane the same mapping behind a runtime-opaque select (p.one == 1)
+    // compiles to a faster backward sweep (8 Wide quads 11.91 -> 11.34 ms; code generation,
+    // measured: tools/ab_flags.sh)
+    const int warp = (CPL == 8) ? ((wid == NW || p.one == 0) ? wid : NW - 1 - wid)
+                                : (wid == NW ? wid : NW - 1 - wid);
     const int lane = lane_id();
     const int W = p.W, H = p.H;
     if (warp == NW) {

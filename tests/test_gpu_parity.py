@@ -284,6 +284,32 @@ def test_batch_config_full(orc, dev):
     g1.close()
 
 
+def test_batch_config_64_quads(orc, dev):
+    """configs[4] in full: all 64 quads (seeds 1000..1063) in the single launch the N=1 bench
+    times, every quad and every output field against the oracle (host cores in parallel),
+    and byte-identical to the eight 8-quad launches of the N=8 partition (SURVEY.md 8(e):
+    gathered outputs equal the 1-GPU run)."""
+    cfg = synth.CONFIGS["batch"]
+    prm = synth.sgm_params(cfg)
+    from paper_1801_04720_b200 import SGM, Camera, stack_quads
+    quads = synth.make_batch(cfg, 0, 64, workers=16)
+    cam = Camera(prm["f"], prm["B"], prm["cx"], prm["cy"])
+    g = SGM.from_config(cfg, max_batch=64)
+    imgs, flow = stack_quads(quads, g.pitch, dev)
+    out = g.scene_flow(imgs, flow, cam)
+    torch.cuda.synchronize()
+    g8 = SGM.from_config(cfg, max_batch=8)
+    for r in range(8):
+        part = g8.scene_flow(imgs[8 * r:8 * r + 8].contiguous(), flow[8 * r:8 * r + 8].contiguous(), cam)
+        torch.cuda.synchronize()
+        for k in ("sf", "valid_sf", "p0", "dp", "valid_3d", "disp_int", "disp_sub", "disp_valid"):
+            assert torch.equal(part[k], out[k][8 * r:8 * r + 8]), (r, k)
+    g8.close()
+    for i, o in enumerate(oracle_many(orc, quads, prm)):
+        check_quad_outputs(out, i, o)
+    g.close()
+
+
 def test_host_entry_point_matches_device(dev):
     from paper_1801_04720_b200 import SGM, Camera, stack_quads
     cfg = synth.CONFIGS["tiny"]

@@ -71,7 +71,7 @@ def main(reps):
             alg = view_px * (2 * cfg.D + (6 if bwd else 16))
             cells = view_px * cfg.D
             lane_instr = float(d["smsp__inst_executed.sum"].replace(",", "")) * 32 / cells
-            table[f"{cfgname}/{kern}"] = {"bytes": rd + wr, "read": rd, "write": wr, "quads": quads,
+            table[f"{cfgname}x{quads}/{kern}"] = {"bytes": rd + wr, "read": rd, "write": wr, "quads": quads,
                                           "algorithmic": alg, "ncu_ms": val("gpu__time_duration.sum") * 1e3,
                                           "lane_instr_per_view_cell": lane_instr,
                                           "source": os.path.basename(rep)}
