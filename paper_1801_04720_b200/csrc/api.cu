@@ -163,6 +163,18 @@ void band_geometry(int H, int nviews, int nsm, int *nbands, int *q, int *r) {
     *r = H % nb;
 }
 
+// Views per ticket group of the sweeps (SweepParams::vgroup).  SGM_VIEW_GROUP
+// (environment, experiments) forces it.
+int view_group(int nviews, int nbands, int nsm) {
+    static const int forced = [] {
+        const char *e = getenv("SGM_VIEW_GROUP");
+        return e ? atoi(e) : 0;
+    }();
+    (void)nbands; (void)nsm;
+    int g = forced > 0 ? forced : nviews;
+    return g < nviews ? g : nviews;
+}
+
 sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int *sync = nullptr) {
     sgm::SweepParams p{};
     const long long v0 = 0;
@@ -170,6 +182,7 @@ sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int *sync = nullp
     p.P1 = h->prm.p1; p.P2 = h->prm.p2; p.cmax = h->cmax;
     p.nviews = nviews;
     band_geometry(p.H, nviews, h->nsm, &p.nbands, &p.band_q, &p.band_r);
+    p.vgroup = view_group(nviews, p.nbands, h->nsm);
     p.cen = h->census + v0 * h->npx; p.cen_img_stride = h->npx;
     p.explicit_mode = 0;
     p.sfwd = h->sfwd + v0 * h->npx * h->dp; p.sfwd_view_stride = h->npx * h->dp;

@@ -25,6 +25,7 @@ struct SweepParams {
     int P1, P2, cmax;
     int nviews, nbands;
     int band_q, band_r;       // band b has band_q + (b < band_r) rows, from row b*band_q + min(b, band_r)
+    int vgroup;               // ticket order: groups of vgroup views, band-major inside a group
     // census images [img][H][W]; batch views: view v -> pair v/2, side v%2
     //   side 0: ref = img 2*(v/2), match = img 2*(v/2)+1, mirror 0 (left reference)
     //   side 1: ref = img 2*(v/2)+1, match = img 2*(v/2), mirror 1 (right reference)

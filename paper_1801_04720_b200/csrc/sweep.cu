@@ -121,9 +121,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
     // forward CTA has started (so they never hold an SM a forward CTA still needs); they
     // then wait per view on fwd_done, not for the whole forward grid.
     if (!BWD) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    // ticket -> (band, view): views in groups of p.vgroup, band-major inside a group, so
+    // that band b+1 of a view starts about one band lag after band b (its handoff rows are
+    // read while still in L2) and never before it (a band only waits for a running band)
     const int ticket = s_ticket;
-    const int band = ticket / p.nviews;
-    const int view = ticket - band * p.nviews;
+    const int grp = ticket / (p.vgroup * p.nbands);
+    const int v0 = grp * p.vgroup;
+    const int gv = min(p.vgroup, p.nviews - v0);
+    const int rem = ticket - v0 * p.nbands;
+    const int band = rem / gv;
+    const int view = v0 + rem - band * gv;
 
     // warp index through a warp reduction: the compiler then keeps it (and everything
     // derived from it) in uniform registers and emits uniform branches.
