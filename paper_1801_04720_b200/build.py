@@ -46,6 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
     extra = ["-Xptxas", "-v"] if verbose else []
+    extra += os.environ.get("SGM_NVCC_EXTRA", "").split()      # A/B variants (tools/)
     for src in sources():
         obj = os.path.join(LIBDIR, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-dc" if False else "-c",

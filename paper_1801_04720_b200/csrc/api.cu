@@ -141,17 +141,19 @@ void band_geometry(int H, int nviews, int nsm, int *nbands, int *q, int *r) {
         const char *e = getenv("SGM_BAND_ROWS");
         return e ? atoi(e) : 0;
     }();
+    constexpr int hi = sgm::kBandRowsMax, lo = hi > sgm::kBandRowsMin ? hi - 1 : hi;
+    nsm *= sgm::kSweepCtasPerSm;                   // CTA slots
     auto bands = [&](int rows) { return (H + rows - 1) / rows; };
     auto waves = [&](int nb) { return ((long long)nviews * nb + nsm - 1) / nsm; };
     int nb;
     if (forced >= sgm::kBandRowsMin && forced <= sgm::kBandRowsMax) {
         nb = bands(forced);
-    } else if ((long long)nviews * bands(16) >= 2LL * nsm) {
-        nb = waves(bands(17)) < waves(bands(16)) ? bands(17) : bands(16);
+    } else if ((long long)nviews * bands(lo) >= 2LL * nsm) {
+        nb = waves(bands(hi)) < waves(bands(lo)) ? bands(hi) : bands(lo);
     } else {
-        nb = bands(16);
+        nb = bands(lo);
         double best = -1.0;
-        for (int rows = 16; rows >= sgm::kBandRowsMin; --rows) {
+        for (int rows = lo; rows >= sgm::kBandRowsMin; --rows) {
             const int n = bands(rows), bq = H / n, br = H % n;
             auto t = [](int h) { return h / 16.0 * (1.0 + 0.012 * (16 - h)); };
             const double cost = double(waves(n)) * ((n - br) * t(bq) + br * t(bq + 1)) / n;

@@ -8,16 +8,31 @@
 namespace sgm {
 
 // ----------------------------------------------------------------- constants
+// (the SGM_* macros select A/B variants of the sweep geometry; the defaults are the product)
+#ifndef SGM_NW
+#define SGM_NW 17
+#endif
+#ifndef SGM_RING_WIDE
+#define SGM_RING_WIDE 16
+#endif
+#ifndef SGM_G_WIDE
+#define SGM_G_WIDE 0
+#endif
+#ifndef SGM_MINB
+#define SGM_MINB 1
+#endif
 constexpr int kRing = 8;        // row->row handoff ring (positions) for CPL > 4
-constexpr int kRingWide = 16;   // ... for CPL <= 4 (fits 16 warps x 16 x 3 x 256 B)
+constexpr int kRingWide = SGM_RING_WIDE;   // ... for CPL <= 4 (fits 16 warps x 16 x 3 x 256 B)
+constexpr int kGroupWide = SGM_G_WIDE;     // ring sync group for CPL <= 4 (0: CPL positions)
+constexpr int kSweepCtasPerSm = SGM_MINB;  // resident sweep CTAs per SM
 constexpr int kRing0 = 16;      // band-input ring of warp 0 (positions)
 constexpr int kPublish = 8;     // forward sweep's band-output publication granularity (positions)
 constexpr int kPubDepth = 4;    // producer -> publisher-warp handoff depth (groups)
 // SGM sweep bands: a CTA carries one band of up to kBandRowsMax rows (one compute warp per
 // row); the host picks the band height per call in [kBandRowsMin, kBandRowsMax] so that
 // the CTA count fills whole waves of the SMs (band_geometry in api.cu)
-constexpr int kBandRowsMax = 17;
-constexpr int kBandRowsMin = 10;
+constexpr int kBandRowsMax = SGM_NW;
+constexpr int kBandRowsMin = SGM_NW < 10 ? SGM_NW : 10;
 
 // ----------------------------------------------------------------- kernel params
 struct SweepParams {

@@ -36,9 +36,30 @@
 
 #include "sweep_common.cuh"
 
+// Row -> row ring synchronisation: 1 (default) = one named barrier per warp pair (ids 0..15:
+// the producer row's index), met once per position group as a rendezvous -- bar.sync blocks
+// in hardware, so a waiting row spends no issue slots; 0 = full / empty mbarriers per ring
+// group (the waiting row spins on try_wait: ncu counted ~89 try_wait retries per group wait,
+// ~20 % of the sweeps' issued instructions).  Measured (1x B200, same box): 64 quads 49.29 ->
+// 47.81 ms, 8 Driving 6.75 -> 6.55, 8 Wide 11.26 -> 10.69, 4 HighRes 20.32 -> 19.65; a producer
+// one group further ahead (SGM_NAMED_LEAD=1) was slower (48.48 ms).
+#ifndef SGM_NAMED_RING
+#define SGM_NAMED_RING 1
+#endif
+#ifndef SGM_PUB_SLEEP
+#define SGM_PUB_SLEEP 0
+#endif
+#ifndef SGM_NAMED_LEAD
+#define SGM_NAMED_LEAD 0
+#endif
+
 namespace sgm {
 namespace {
 using namespace sweep_detail;
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 template <int CPL, bool C64, bool BWD, int NW>
 struct Sweep {
@@ -52,7 +73,7 @@ struct Sweep {
     static constexpr int RS = (CPL <= 4) ? kRingWide : kRing;
     // groups align with the unrolled block; CPL > 4 (8 ring slots): 2-position groups
     // (lead window [3, 6]) instead of per-position sync: Wide 15.6 -> 11.5 ms
-    static constexpr int G = (CPL <= 4) ? CPL : 2;
+    static constexpr int G = (CPL <= 4) ? (kGroupWide ? kGroupWide : CPL) : 2;
     static constexpr int RG = RS / G;              // groups per ring
     // band-input ring of warp 0 (positions) and census prefetch entries per warp: trimmed
     // for 8 cells per lane so that 17-row bands fit the 227 KB of shared memory
@@ -75,8 +96,9 @@ struct Sweep {
 
 // SOUT (backward sweep only): write S(d) of view 0 (sgm_aggregate, debug) instead of WTA
 template <int CPL, bool C64, bool BWD, int NW, bool PAD, bool SOUT>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepParams p) {
+__global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(const SweepParams p) {
     using SW = Sweep<CPL, C64, BWD, NW>;
+    static_assert(!SGM_NAMED_RING || NW <= 17, "named ring barriers: ids 0..NW-2 must be < 16");
     // band-handoff publication granularity (positions): measured best 8 for the forward
     // sweep, 4 for the backward sweep
     constexpr int PUB = BWD ? 4 : kPublish;
@@ -163,7 +185,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             constexpr int kLinesPerPos = 3 * DP * 2 / 128;
             const int ngroups = (W + PUB - 1) / PUB;
             for (int k = 0; k < ngroups; ++k) {
+#if SGM_PUB_SLEEP
+                // back off between tests: a spinning publisher takes issue slots from the
+                // compute warps of its SM sub-partition
+                while (!mbar_test(pub_full + (k % kPubDepth), unsigned(k / kPubDepth) & 1u))
+                    __nanosleep(SGM_PUB_SLEEP);
+#else
                 mbar_wait(pub_full + (k % kPubDepth), unsigned(k / kPubDepth) & 1u);
+#endif
                 asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
                 if (lane == 0) {
                     st_relaxed_gpu(prog, min((k + 1) * PUB, W));
@@ -395,7 +424,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
                 }
             } else if (ring_input && (ph % G) == 0) {
                 const int g = i / G;                       // group start: wait for slots
-                mbar_wait(src_full + (g % RG), unsigned(g / RG) & 1u);
+                if (SGM_NAMED_RING) named_sync(warp - 1, 64);   // rendezvous g
+                else mbar_wait(src_full + (g % RG), unsigned(g / RG) & 1u);
             }
             // --- census prefetch refill
             if (BWD) {
@@ -483,7 +513,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
 #pragma unroll
                 for (int v = 0; v < 3; ++v) VecIO<R>::ld(src + v * DP, pv[v]);
             }
-            if (ring_input && (ph % G) == G - 1) {       // group end: release its slots
+            if (!SGM_NAMED_RING && ring_input && (ph % G) == G - 1) {   // group end: release its slots
                 __syncwarp();
                 mbar_arrive(src_empty + ((i / G) % RG));
             }
@@ -504,14 +534,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
             for (int r = 0; r < R; ++r) S[r] = (S[r] + nv[0][r] + nv[1][r]) + (nv[2][r] + negb4);
             // --- hand the three vectors to the row below
             if (has_row_below) {
-                if ((ph % G) == G - 1) {                   // next group's slots free again?
+                if (!SGM_NAMED_RING && (ph % G) == G - 1) {   // next group's slots free again?
                     const int h = i / G + 1;
                     if (h >= RG) mbar_wait(my_empty + (h % RG), unsigned(h / RG - 1) & 1u);
                 }
                 VecIO<R>::st(my_ring + size_t(i & (RS - 1)) * VEC, nv[0]);
                 VecIO<R>::st(my_ring + size_t((i + 1) & (RS - 1)) * VEC + DP, nv[1]);
                 VecIO<R>::st(my_ring + size_t((i - 1) & (RS - 1)) * VEC + 2 * DP, nv[2]);
-                if ((ph % G) == 0 && i > 0) mbar_arrive(my_full + ((i / G - 1) % RG));   // group done
+                if (SGM_NAMED_RING) {
+                    // rendezvous n = i/G - 1 - lead once position (n + 1 + lead) G is stored
+                    if ((ph % G) == 0 && i >= (1 + SGM_NAMED_LEAD) * G) named_sync(warp, 64);
+                } else if ((ph % G) == 0 && i > 0) {
+                    mbar_arrive(my_full + ((i / G - 1) % RG));   // group done
+                }
             } else if (is_producer) {
                 uint16_t *g = gout + (long long)i * VEC;
                 uint32_t zero[R];
@@ -609,7 +644,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const SweepPara
 #pragma unroll
         for (int r = 0; r < R; ++r) zero[r] = p1x2;                // biased path start
         VecIO<R>::st(my_ring + size_t((W - 1) & (RS - 1)) * VEC + 2 * DP, zero);
-        mbar_arrive(my_full + (((W - 1) / G) % RG));
+        if (SGM_NAMED_RING) {
+            // the consumer meets ceil(W / G) rendezvous; the loop made floor((W-1)/G) - lead
+            const int ng = (W + G - 1) / G;
+            int done = (W - 1) / G - SGM_NAMED_LEAD;
+            for (done = done < 0 ? 0 : done; done < ng; ++done) named_sync(warp, 64);
+        } else {
+            mbar_arrive(my_full + (((W - 1) / G) % RG));
+        }
     }
     if (band_input) cp_async_wait<0>();
     if (band_input && known >= (1 << 30)) fault(kFaultBandInput);

@@ -164,5 +164,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
         : "memory");
 }
 
+// One mbarrier test (no retry loop): true once the phase with `parity` has completed.
+__device__ __forceinline__ bool mbar_test(uint64_t *b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 }  // namespace sweep_detail
 }  // namespace sgm
