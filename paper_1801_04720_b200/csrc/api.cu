@@ -182,9 +182,16 @@ sgm::SweepParams sweep_params(const sgm_handle *h, int nviews, int *sync = nullp
     const long long v0 = 0;
     p.W = h->prm.width; p.H = h->prm.height; p.D = h->prm.num_disp; p.Dp = h->dp;
     p.P1 = h->prm.p1; p.P2 = h->prm.p2; p.cmax = h->cmax;
+    p.k_p1x2 = uint32_t(p.P1) * 0x10001u;
+    p.k_negp1x2 = (uint32_t(0x10000 - p.P1) & 0xFFFFu) * 0x10001u;
+    p.k_p2mp1x2 = uint32_t(p.P2 - p.P1) * 0x10001u;
+    p.k_twop1x2 = 2u * p.k_p1x2;
+    p.k_negb4 = 0u - 4u * p.k_p1x2;
     p.nviews = nviews;
     band_geometry(p.H, nviews, h->nsm, &p.nbands, &p.band_q, &p.band_r);
     p.vgroup = view_group(nviews, p.nbands, h->nsm);
+    p.fine_sync = (long long)nviews * p.nbands < 2LL * h->nsm * sgm::kSweepCtasPerSm ? 1 : 0;
+    if (const char *e = getenv("SGM_FINE_SYNC")) p.fine_sync = atoi(e);   // experiments
     p.cen = h->census + v0 * h->npx; p.cen_img_stride = h->npx;
     p.explicit_mode = 0;
     p.sfwd = h->sfwd + v0 * h->npx * h->dp; p.sfwd_view_stride = h->npx * h->dp;

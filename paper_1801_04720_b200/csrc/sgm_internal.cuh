@@ -25,6 +25,10 @@ constexpr int kRing = 8;        // row->row handoff ring (positions) for CPL > 4
 constexpr int kRingWide = SGM_RING_WIDE;   // ... for CPL <= 4 (fits 16 warps x 16 x 3 x 256 B)
 constexpr int kGroupWide = SGM_G_WIDE;     // ring sync group for CPL <= 4 (0: CPL positions)
 constexpr int kSweepCtasPerSm = SGM_MINB;  // resident sweep CTAs per SM
+#ifndef SGM_FINE_GROUP
+#define SGM_FINE_GROUP 1
+#endif
+constexpr int kFineGroup = SGM_FINE_GROUP; // ring sync group of the latency mode (CPL <= 4)
 constexpr int kRing0 = 16;      // band-input ring of warp 0 (positions)
 constexpr int kPublish = 8;     // forward sweep's band-output publication granularity (positions)
 constexpr int kPubDepth = 4;    // producer -> publisher-warp handoff depth (groups)
@@ -41,6 +45,10 @@ struct SweepParams {
     int nviews, nbands;
     int band_q, band_r;       // band b has band_q + (b < band_r) rows, from row b*band_q + min(b, band_r)
     int vgroup;               // ticket order: groups of vgroup views, band-major inside a group
+    int fine_sync;            // latency mode (< 2 waves of CTAs): finer row-to-row sync groups
+    // u16x2 constants of the path update, precomputed on the host (kernel-parameter operands
+    // instead of per-lane registers): P1, -P1, P2 - P1, 2 P1 in both halves, -4 P1 (S bias)
+    uint32_t k_p1x2, k_negp1x2, k_p2mp1x2, k_twop1x2, k_negb4;
     // census images [img][H][W]; batch views: view v -> pair v/2, side v%2
     //   side 0: ref = img 2*(v/2), match = img 2*(v/2)+1, mirror 0 (left reference)
     //   side 1: ref = img 2*(v/2)+1, match = img 2*(v/2), mirror 1 (right reference)

@@ -46,6 +46,15 @@
 #ifndef SGM_NAMED_RING
 #define SGM_NAMED_RING 1
 #endif
+#ifndef SGM_TAIL_SPLIT
+#define SGM_TAIL_SPLIT 1
+#endif
+#ifndef SGM_SLOT_BASE
+#define SGM_SLOT_BASE 1
+#endif
+#ifndef SGM_CONST_PARAMS
+#define SGM_CONST_PARAMS 0
+#endif
 #ifndef SGM_PUB_SLEEP
 #define SGM_PUB_SLEEP 0
 #endif
@@ -61,7 +70,8 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int CPL, bool C64, bool BWD, int NW>
+// GS: ring sync group (positions) for CPL <= 4; 0 = the default (kGroupWide, else CPL)
+template <int CPL, bool C64, bool BWD, int NW, int GS = 0>
 struct Sweep {
     static constexpr int R = CPL / 2;
     static constexpr int DP = 32 * CPL;
@@ -73,7 +83,7 @@ struct Sweep {
     static constexpr int RS = (CPL <= 4) ? kRingWide : kRing;
     // groups align with the unrolled block; CPL > 4 (8 ring slots): 2-position groups
     // (lead window [3, 6]) instead of per-position sync: Wide 15.6 -> 11.5 ms
-    static constexpr int G = (CPL <= 4) ? (kGroupWide ? kGroupWide : CPL) : 2;
+    static constexpr int G = (CPL <= 4) ? (GS ? GS : (kGroupWide ? kGroupWide : CPL)) : 2;
     static constexpr int RG = RS / G;              // groups per ring
     // band-input ring of warp 0 (positions) and census prefetch entries per warp: trimmed
     // for 8 cells per lane so that 17-row bands fit the 227 KB of shared memory
@@ -95,10 +105,12 @@ struct Sweep {
 };
 
 // SOUT (backward sweep only): write S(d) of view 0 (sgm_aggregate, debug) instead of WTA
-template <int CPL, bool C64, bool BWD, int NW, bool PAD, bool SOUT>
+template <int CPL, bool C64, bool BWD, int NW, bool PAD, bool SOUT, int GS>
 __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(const SweepParams p) {
-    using SW = Sweep<CPL, C64, BWD, NW>;
+    using SW = Sweep<CPL, C64, BWD, NW, GS>;
     static_assert(!SGM_NAMED_RING || NW <= 17, "named ring barriers: ids 0..NW-2 must be < 16");
+    // block-relative ring slots (needs the loop split into whole CPL blocks)
+    constexpr bool SB = SGM_SLOT_BASE && SGM_TAIL_SPLIT && (SW::RS % CPL == 0) && (SW::RING0 % CPL == 0);
     // band-handoff publication granularity (positions): measured best 8 for the forward
     // sweep, 4 for the backward sweep
     constexpr int PUB = BWD ? 4 : kPublish;
@@ -267,11 +279,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
 
     // per-lane constants
     const uint32_t one = uint32_t(p.one);
+#if SGM_CONST_PARAMS
+    const uint32_t p1x2 = p.k_p1x2, negp1x2 = p.k_negp1x2, p2mp1x2 = p.k_p2mp1x2;
+    const uint32_t twop1x2 = p.k_twop1x2, negb4 = p.k_negb4;
+#else
     const uint32_t p1x2 = uint32_t(p.P1) * 0x10001u;
     const uint32_t negp1x2 = (uint32_t(0x10000 - p.P1) & 0xFFFFu) * 0x10001u;   // -P1 per half
     const uint32_t p2mp1x2 = uint32_t(p.P2 - p.P1) * 0x10001u;                  // P2 - P1
     const uint32_t twop1x2 = 2u * p1x2;
     const uint32_t negb4 = 0u - 4u * p1x2;            // removes the 4 path biases from S
+#endif
     const int dbase = CPL * lane;                  // the lane's u16 offset inside a vector
     // folded layout (path_update): register r holds disparities dlo + r (low half) and
     // dhi - r (high half)
@@ -408,12 +425,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
         trace[2] = sm;
     }
 
+#if SGM_TAIL_SPLIT
+    // one position of the row (ph = i mod CPL is a compile-time constant after unrolling)
+    auto position = [&](const int i0, const int ph) {
+        {
+            const int i = i0 + ph;
+#else
 #pragma unroll 1
     for (int i0 = 0; i0 < W; i0 += CPL) {
 #pragma unroll
         for (int ph = 0; ph < CPL; ++ph) {
             const int i = i0 + ph;
             if (i >= W) break;
+#endif
             const int xv = xview(i);
             // --- inputs of the row above
             if (band_input) {
@@ -509,7 +533,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
             // --- row-above predecessors: all three live in slot i
             uint32_t pv[3][R];
             {
-                const uint16_t *src = src_ring + size_t(i & (band_input || warp == 0 ? RING0 - 1 : RS - 1)) * VEC;
+                // block-relative slots (SB): i0 is a multiple of CPL and CPL divides the ring
+                const int msk = band_input || warp == 0 ? RING0 - 1 : RS - 1;
+                const uint16_t *src = src_ring + size_t(SB ? (i0 & msk) + ph : (i & msk)) * VEC;
 #pragma unroll
                 for (int v = 0; v < 3; ++v) VecIO<R>::ld(src + v * DP, pv[v]);
             }
@@ -538,9 +564,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                     const int h = i / G + 1;
                     if (h >= RG) mbar_wait(my_empty + (h % RG), unsigned(h / RG - 1) & 1u);
                 }
-                VecIO<R>::st(my_ring + size_t(i & (RS - 1)) * VEC, nv[0]);
-                VecIO<R>::st(my_ring + size_t((i + 1) & (RS - 1)) * VEC + DP, nv[1]);
-                VecIO<R>::st(my_ring + size_t((i - 1) & (RS - 1)) * VEC + 2 * DP, nv[2]);
+                {
+                    const int sb = i0 & (RS - 1);
+                    const int s0 = SB ? sb + ph : (i & (RS - 1));
+                    const int s1 = SB ? ((ph == CPL - 1) ? ((i0 + CPL) & (RS - 1)) : sb + ph + 1) : ((i + 1) & (RS - 1));
+                    const int s2 = SB ? ((ph == 0) ? ((i0 - 1) & (RS - 1)) : sb + ph - 1) : ((i - 1) & (RS - 1));
+                    VecIO<R>::st(my_ring + size_t(s0) * VEC, nv[0]);
+                    VecIO<R>::st(my_ring + size_t(s1) * VEC + DP, nv[1]);
+                    VecIO<R>::st(my_ring + size_t(s2) * VEC + 2 * DP, nv[2]);
+                }
                 if (SGM_NAMED_RING) {
                     // rendezvous n = i/G - 1 - lead once position (n + 1 + lead) G is stored
                     if ((ph % G) == 0 && i >= (1 + SGM_NAMED_LEAD) * G) named_sync(warp, 64);
@@ -637,6 +669,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
             }
         }
     }
+#if SGM_TAIL_SPLIT
+    ;
+    // whole CPL-position blocks without a per-position bound check, then the tail
+    const int Wfull = W - W % CPL;
+#pragma unroll 1
+    for (int i0 = 0; i0 < Wfull; i0 += CPL) {
+#pragma unroll
+        for (int ph = 0; ph < CPL; ++ph) position(i0, ph);
+    }
+    if (Wfull < W) {
+#pragma unroll
+        for (int ph = 0; ph < CPL - 1; ++ph)
+            if (Wfull + ph < W) position(Wfull, ph);
+    }
+#endif
     if (has_row_below) {
         // position W lies outside the image: the (-1,1) path of the row below starts at
         // x' = W-1, so that slot's v2 must read as zero; then release slot W-1.
@@ -673,7 +720,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
 //   [ticket, progress[nviews*nbands]] forward, the same for the backward sweep, fwd_done[nviews]
 // and the band-handoff buffer is split in two, so that the backward sweep (launched with
 // programmatic stream serialisation) can overlap the forward sweep's last wave.
-template <int CPL, bool C64, int NW, bool PAD>
+template <int CPL, bool C64, int NW, bool PAD, int GS>
 cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cudaEvent_t ev_mid_a,
                         cudaEvent_t ev_mid_b, int *launches, int *sync_buf, size_t sync_bytes) {
     (void)debug_s;
@@ -687,8 +734,8 @@ cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cud
     cudaError_t e;
     if ((e = cudaMemsetAsync(sync_buf, 0, sync_bytes, st)) != cudaSuccess) return e;
     {
-        constexpr size_t sm = Sweep<CPL, C64, false, NW>::smem_bytes();
-        auto k = sweep_kernel<CPL, C64, false, NW, PAD, false>;
+        constexpr size_t sm = Sweep<CPL, C64, false, NW, GS>::smem_bytes();
+        auto k = sweep_kernel<CPL, C64, false, NW, PAD, false, GS>;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))) != cudaSuccess) return e;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
         k<<<grid, block, sm, st>>>(pf);
@@ -698,10 +745,10 @@ cudaError_t launch_pair(const SweepParams &p, bool debug_s, cudaStream_t st, cud
     if (ev_mid_a) cudaEventRecord(ev_mid_a, st);    // (timing mode: no overlap)
     if (ev_mid_b) cudaEventRecord(ev_mid_b, st);
     {
-        constexpr size_t sm = Sweep<CPL, C64, true, NW>::smem_bytes();   // same for PAD
+        constexpr size_t sm = Sweep<CPL, C64, true, NW, GS>::smem_bytes();   // same for PAD
         // the backward sweep keeps the general (padded) cost unpack: specialising it for
         // D = Dp measured slower (3.78 -> 3.94 ms on 8 Driving quads; code scheduling)
-        auto k = p.sout ? sweep_kernel<CPL, C64, true, NW, true, true> : sweep_kernel<CPL, C64, true, NW, true, false>;
+        auto k = p.sout ? sweep_kernel<CPL, C64, true, NW, true, true, GS> : sweep_kernel<CPL, C64, true, NW, true, false, GS>;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))) != cudaSuccess) return e;
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
         cudaLaunchConfig_t cfg = {};
@@ -733,16 +780,22 @@ cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool 
     int *sync_buf = p.ticket;
     const size_t sync_bytes = sizeof(int) * sweep_sync_ints(p.nviews, p.nbands);
     if (nw != sweep_warps_for(cpl)) return cudaErrorInvalidValue;
+#define SGM_PAIR(CPL_, C64_, PAD_, GS_)                                                        \
+    launch_pair<CPL_, C64_, kBandRowsMax, PAD_, GS_>(p, debug_s, st, mid_ev_a, mid_ev_b, launches, \
+                                                   sync_buf, sync_bytes)
+    // latency mode (fewer than two waves of CTAs: each view's band chain is the critical
+    // path): CPL <= 4 rows meet every kFineGroup positions instead of every CPL (a shorter
+    // row-to-row lag shortens the chain)
 #define SGM_CASE(CPL_, C64_)                                                                   \
     if (cpl == CPL_ && c64 == C64_) {                                                          \
+        constexpr int gf = CPL_ <= 4 ? kFineGroup : 0;                                         \
         if (p.D < 32 * CPL_)                                                                   \
-            return launch_pair<CPL_, C64_, kBandRowsMax, true>(                        \
-                p, debug_s, st, mid_ev_a, mid_ev_b, launches, sync_buf, sync_bytes);           \
-        return launch_pair<CPL_, C64_, kBandRowsMax, false>(                           \
-            p, debug_s, st, mid_ev_a, mid_ev_b, launches, sync_buf, sync_bytes);               \
+            return p.fine_sync && gf ? SGM_PAIR(CPL_, C64_, true, gf) : SGM_PAIR(CPL_, C64_, true, 0); \
+        return p.fine_sync && gf ? SGM_PAIR(CPL_, C64_, false, gf) : SGM_PAIR(CPL_, C64_, false, 0);   \
     }
     SGM_CASE(2, false) SGM_CASE(2, true) SGM_CASE(4, false) SGM_CASE(4, true)
     SGM_CASE(6, false) SGM_CASE(6, true) SGM_CASE(8, false) SGM_CASE(8, true)
+#undef SGM_PAIR
 #undef SGM_CASE
     return cudaErrorInvalidValue;
 }
