@@ -52,8 +52,14 @@
 #ifndef SGM_SLOT_BASE
 #define SGM_SLOT_BASE 1
 #endif
+#ifndef SGM_FINE_PUB
+#define SGM_FINE_PUB 0
+#endif
+#ifndef SGM_FINE_ALL
+#define SGM_FINE_ALL 0
+#endif
 #ifndef SGM_CONST_PARAMS
-#define SGM_CONST_PARAMS 0
+#define SGM_CONST_PARAMS 1
 #endif
 #ifndef SGM_PUB_SLEEP
 #define SGM_PUB_SLEEP 0
@@ -69,6 +75,9 @@ using namespace sweep_detail;
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // GS: ring sync group (positions) for CPL <= 4; 0 = the default (kGroupWide, else CPL)
 template <int CPL, bool C64, bool BWD, int NW, int GS = 0>
@@ -83,7 +92,7 @@ struct Sweep {
     static constexpr int RS = (CPL <= 4) ? kRingWide : kRing;
     // groups align with the unrolled block; CPL > 4 (8 ring slots): 2-position groups
     // (lead window [3, 6]) instead of per-position sync: Wide 15.6 -> 11.5 ms
-    static constexpr int G = (CPL <= 4) ? (GS ? GS : (kGroupWide ? kGroupWide : CPL)) : 2;
+    static constexpr int G = GS ? GS : ((CPL <= 4) ? (kGroupWide ? kGroupWide : CPL) : 2);
     static constexpr int RG = RS / G;              // groups per ring
     // band-input ring of warp 0 (positions) and census prefetch entries per warp: trimmed
     // for 8 cells per lane so that 17-row bands fit the 227 KB of shared memory
@@ -113,7 +122,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
     constexpr bool SB = SGM_SLOT_BASE && SGM_TAIL_SPLIT && (SW::RS % CPL == 0) && (SW::RING0 % CPL == 0);
     // band-handoff publication granularity (positions): measured best 8 for the forward
     // sweep, 4 for the backward sweep
-    constexpr int PUB = BWD ? 4 : kPublish;
+    constexpr int PUB = (GS && SGM_FINE_PUB) ? SGM_FINE_PUB : (BWD ? 4 : kPublish);
     constexpr int R = SW::R;
     constexpr int DP = SW::DP;
     constexpr int VEC = SW::VEC;
@@ -279,16 +288,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
 
     // per-lane constants
     const uint32_t one = uint32_t(p.one);
-#if SGM_CONST_PARAMS
-    const uint32_t p1x2 = p.k_p1x2, negp1x2 = p.k_negp1x2, p2mp1x2 = p.k_p2mp1x2;
-    const uint32_t twop1x2 = p.k_twop1x2, negb4 = p.k_negb4;
-#else
-    const uint32_t p1x2 = uint32_t(p.P1) * 0x10001u;
-    const uint32_t negp1x2 = (uint32_t(0x10000 - p.P1) & 0xFFFFu) * 0x10001u;   // -P1 per half
-    const uint32_t p2mp1x2 = uint32_t(p.P2 - p.P1) * 0x10001u;                  // P2 - P1
-    const uint32_t twop1x2 = 2u * p1x2;
-    const uint32_t negb4 = 0u - 4u * p1x2;            // removes the 4 path biases from S
-#endif
+    // the forward sweep takes the u16x2 constants as kernel-parameter operands (c[] bank:
+    // forward sweep 21.38 -> 21.03 ms on 64 quads); the backward sweep computes them into
+    // registers (as parameters it measured slower: 21.32 -> 21.46 ms, Wide 5.29 -> 5.87 ms)
+    constexpr bool kcp = SGM_CONST_PARAMS && !BWD;
+    const uint32_t p1x2 = kcp ? p.k_p1x2 : uint32_t(p.P1) * 0x10001u;
+    const uint32_t negp1x2 = kcp ? p.k_negp1x2 : (uint32_t(0x10000 - p.P1) & 0xFFFFu) * 0x10001u;   // -P1 per half
+    const uint32_t p2mp1x2 = kcp ? p.k_p2mp1x2 : uint32_t(p.P2 - p.P1) * 0x10001u;                  // P2 - P1
+    const uint32_t twop1x2 = kcp ? p.k_twop1x2 : 2u * p1x2;
+    const uint32_t negb4 = kcp ? p.k_negb4 : 0u - 4u * p1x2;    // removes the 4 path biases from S
     const int dbase = CPL * lane;                  // the lane's u16 offset inside a vector
     // folded layout (path_update): register r holds disparities dlo + r (low half) and
     // dhi - r (high half)
@@ -448,7 +456,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                 }
             } else if (ring_input && (ph % G) == 0) {
                 const int g = i / G;                       // group start: wait for slots
-                if (SGM_NAMED_RING) named_sync(warp - 1, 64);   // rendezvous g
+                if (SGM_NAMED_RING == 2) {
+                    // blocking wait for the producer's arrival g, then tell it sync g passed
+                    named_sync(warp - 1, 64);
+                    mbar_arrive(src_empty);
+                } else if (SGM_NAMED_RING) {
+                    named_sync(warp - 1, 64);                  // rendezvous g
+                }
                 else mbar_wait(src_full + (g % RG), unsigned(g / RG) & 1u);
             }
             // --- census prefetch refill
@@ -573,7 +587,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                     VecIO<R>::st(my_ring + size_t(s1) * VEC + DP, nv[1]);
                     VecIO<R>::st(my_ring + size_t(s2) * VEC + 2 * DP, nv[2]);
                 }
-                if (SGM_NAMED_RING) {
+                if (SGM_NAMED_RING == 2) {
+                    // arrival n = i/G - 1 once position (n + 1) G is stored, after the consumer
+                    // passed its sync n - 1 (at most one arrival pending per barrier id)
+                    if ((ph % G) == 0 && i >= G) {
+                        const int n = i / G - 1;
+                        if (n >= 1) mbar_wait(my_empty, unsigned(n - 1) & 1u);
+                        named_arrive(warp, 64);
+                    }
+                } else if (SGM_NAMED_RING) {
                     // rendezvous n = i/G - 1 - lead once position (n + 1 + lead) G is stored
                     if ((ph % G) == 0 && i >= (1 + SGM_NAMED_LEAD) * G) named_sync(warp, 64);
                 } else if ((ph % G) == 0 && i > 0) {
@@ -691,7 +713,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
 #pragma unroll
         for (int r = 0; r < R; ++r) zero[r] = p1x2;                // biased path start
         VecIO<R>::st(my_ring + size_t((W - 1) & (RS - 1)) * VEC + 2 * DP, zero);
-        if (SGM_NAMED_RING) {
+        if (SGM_NAMED_RING == 2) {
+            const int ng = (W + G - 1) / G;
+            for (int n = (W - 1) / G; n < ng; ++n) {
+                if (n >= 1) mbar_wait(my_empty, unsigned(n - 1) & 1u);
+                named_arrive(warp, 64);
+            }
+        } else if (SGM_NAMED_RING) {
             // the consumer meets ceil(W / G) rendezvous; the loop made floor((W-1)/G) - lead
             const int ng = (W + G - 1) / G;
             int done = (W - 1) / G - SGM_NAMED_LEAD;
@@ -788,7 +816,7 @@ cudaError_t launch_sweeps(const SweepParams &p, int cpl, bool c64, int nw, bool 
     // row-to-row lag shortens the chain)
 #define SGM_CASE(CPL_, C64_)                                                                   \
     if (cpl == CPL_ && c64 == C64_) {                                                          \
-        constexpr int gf = CPL_ <= 4 ? kFineGroup : 0;                                         \
+        constexpr int gf = (CPL_ <= 4 || SGM_FINE_ALL) ? kFineGroup : 0;                       \
         if (p.D < 32 * CPL_)                                                                   \
             return p.fine_sync && gf ? SGM_PAIR(CPL_, C64_, true, gf) : SGM_PAIR(CPL_, C64_, true, 0); \
         return p.fine_sync && gf ? SGM_PAIR(CPL_, C64_, false, gf) : SGM_PAIR(CPL_, C64_, false, 0);   \
