@@ -58,6 +58,9 @@
 #ifndef SGM_FINE_ALL
 #define SGM_FINE_ALL 0
 #endif
+#ifndef SGM_WTA_SHFL
+#define SGM_WTA_SHFL 0
+#endif
 #ifndef SGM_CONST_PARAMS
 #define SGM_CONST_PARAMS 1
 #endif
@@ -654,6 +657,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                     }
                     const uint32_t bkey = __reduce_min_sync(0xffffffffu, best);
                     const int dstar = int(bkey & 0xffu);
+#if SGM_WTA_SHFL
+                    // S(d*-1), S(d*+1) straight from the registers of the lanes holding them:
+                    // d lies in pair k = min(d, Dp-1-d) (low half iff d < Dp/2), register k mod
+                    // R of lane k / R (values at d* = 0 / Dp-1 are never used)
+                    auto s_at = [&](int d) -> uint32_t {
+                        const bool lo = d < DP / 2;
+                        const int k = lo ? d : DP - 1 - d;
+                        const int kl = k / R, kr = k - kl * R;
+                        uint32_t v = St[0];
+#pragma unroll
+                        for (int r = 1; r < R; ++r) v = (kr == r) ? St[r] : v;
+                        v = __shfl_sync(0xffffffffu, v, kl & 31);
+                        return lo ? (v & 0xffffu) : (v >> 16);
+                    };
+                    const uint32_t sa = s_at(dstar - 1);
+                    const uint32_t sc = s_at(dstar + 1);
+#else
                     __syncwarp();                                // previous reads of wta done
 #pragma unroll
                     for (int r = 0; r < R; ++r) {           // natural disparity order
@@ -665,6 +685,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                     // d* = 0 / Dp-1)
                     const uint32_t sa = wta[dstar + 1];
                     const uint32_t sc = wta[dstar + 3];
+#endif
                     const int sl = i & 31;
                     if (lane == sl) { rec_key = bkey; rec_ac = sa | (sc << 16); }
                     // every 32 positions each lane finishes one pixel: the parabola

@@ -10,14 +10,14 @@ timeout 1200 python bench.py > gpurun_out/r02_bench.log 2> gpurun_out/r02_bench.
 echo "bench exit $?"
 tail -1 gpurun_out/r02_bench.log > gpurun_out/r02_bench.json
 A="--minimal --no-e2e --no-graph --steps 2 --warmup 3"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+timeout 600 ncu -f --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/r02_launches.csv python bench.py $A > gpurun_out/r02_ncu_list.log 2>&1
 echo "ncu list exit $?"
 # the reports themselves are large: keep the raw-page CSV of each (what tools/ncu_traffic.py
 # reads) and the full report of the 8-quad Driving step only (gpurun_out/ must stay < 64 MiB)
 for spec in "batch 64" "driving 8" "driving 1" "wide 8" "highres 4" "tiny 64"; do
     set -- $spec
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -c 2 \
+    timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:sweep_kernel -c 2 \
         -o gpurun_out/r02_sweep_$1x$2 python tools/sweep_time.py $1 $2 2 > gpurun_out/r02_ncu_$1x$2.log 2>&1
     echo "ncu $1x$2 exit $?"
     ncu -i gpurun_out/r02_sweep_$1x$2.ncu-rep --page raw --csv > gpurun_out/r02_sweep_$1x$2.raw.csv 2>/dev/null
