@@ -35,11 +35,14 @@ print(json.dumps(res))
 """
 
 
-def _run(rows):
+def _run(rows, fine=None):
     env = dict(os.environ)
     env.pop("SGM_BAND_ROWS", None)
+    env.pop("SGM_FINE_SYNC", None)
     if rows:
         env["SGM_BAND_ROWS"] = str(rows)
+    if fine is not None:
+        env["SGM_FINE_SYNC"] = str(fine)
     r = subprocess.run([sys.executable, "-c", CHILD, ROOT], env=env, capture_output=True, text=True,
                        timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -53,3 +56,12 @@ def test_band_heights_bit_identical():
         for k, v in ref.items():
             if k != "band_rows":
                 assert got[k] == v, (rows, k)
+
+
+def test_sync_modes_bit_identical():
+    """Latency mode (rows meet every position, chosen below two waves of CTAs: this 2-quad
+    call) and throughput mode (every CPL positions) give the same bits, for two band heights."""
+    for rows in (0, 16):
+        a, b = _run(rows, fine=1), _run(rows, fine=0)
+        for k, v in a.items():
+            assert b[k] == v, (rows, k)
