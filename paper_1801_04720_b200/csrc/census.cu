@@ -16,6 +16,10 @@
 
 #include "sgm_internal.cuh"
 
+#ifndef SGM_CENSUS_SIMD
+#define SGM_CENSUS_SIMD 1
+#endif
+
 namespace sgm {
 namespace {
 
@@ -79,6 +83,57 @@ __device__ __forceinline__ uint64_t census_px_in(const uint8_t *s, int lx, int l
     return uint64_t(lo) | (uint64_t(hi) << 32);
 }
 
+// Four horizontally adjacent interior pixels (x = 4a .. 4a+3 of the tile row ly) at once,
+// byte-SIMD: the four centres are the bytes of one word C; for each window offset the four
+// neighbours are the bytes of one word N (a PRMT funnel of two aligned row words), and the
+// four comparisons N < C are one unsigned per-byte less-than in three ALU ops:
+//   lt(bit 7 of each byte) = (~n & c) | (~(n ^ c) & ~d),   d = (n | 0x80..) - (c & 0x7f..)
+// (d's byte b has bit 7 set iff n_b mod 128 >= c_b mod 128; no borrow crosses bytes).
+// Window bit k of pixel j goes to bit k % 8 of byte j of acc[k / 8]; a final byte transpose
+// turns acc[0..7] into the four 64-bit census words (byte g = acc[g] byte j).
+template <int CW, int CH>
+__device__ __forceinline__ void census_px4_in(const uint8_t *s, int lx, int ly, uint64_t (&out)[4]) {
+    constexpr int rx = CW / 2, ry = CH / 2;
+    static_assert(rx <= 4, "window wider than 9 needs more row words");
+    constexpr int NB = (CW * CH - 1 + 7) / 8;          // census bytes in use
+    const uint32_t *ctr = reinterpret_cast<const uint32_t *>(s + (ly + ry) * kBoxW + (lx + kHaloX));
+    const uint32_t c = ctr[0];
+    const uint32_t c7f = c & 0x7f7f7f7fu;
+    uint32_t acc[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) acc[g] = 0;
+    int k = 0;
+#pragma unroll
+    for (int dy = -ry; dy <= ry; ++dy) {
+        const uint32_t *row = ctr + dy * (kBoxW / 4);
+        const uint32_t w0 = row[-1], w1 = row[0], w2 = row[1];
+#pragma unroll
+        for (int dx = -rx; dx <= rx; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            // bytes x+dx .. x+dx+3
+            const uint32_t n = dx < 0 ? __byte_perm(w0, w1, 0x3210 + 0x1111 * (4 + dx))
+                                      : (dx == 0 ? w1 : __byte_perm(w1, w2, 0x3210 + 0x1111 * dx));
+            const uint32_t d = (n | 0x80808080u) - c7f;
+            const uint32_t lt = (~n & c) | (~(n ^ c) & ~d);      // bit 7 of each byte
+            const int g = k >> 3, b = k & 7;
+            acc[g] |= (lt >> (7 - b)) & (0x01010101u << b);
+            ++k;
+        }
+    }
+    // byte transpose: out[j] byte g = acc[g] byte j
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t sel = uint32_t(j) | (uint32_t(j + 4) << 4);   // bytes j of (a, b)
+        const uint32_t lo01 = __byte_perm(acc[0], acc[1], sel);
+        const uint32_t lo23 = __byte_perm(acc[2], acc[3], sel);
+        const uint32_t hi45 = NB > 4 ? __byte_perm(acc[4], acc[5], sel) : 0u;
+        const uint32_t hi67 = NB > 6 ? __byte_perm(acc[6], acc[7], sel) : 0u;
+        const uint32_t lo = __byte_perm(lo01, lo23, 0x5410);
+        const uint32_t hi = __byte_perm(hi45, hi67, 0x5410);
+        out[j] = uint64_t(lo) | (uint64_t(hi) << 32);
+    }
+}
+
 template <int CW, int CH>
 __global__ void __launch_bounds__(kThreads) census_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           CensusParams prm, uint64_t *out,
@@ -121,9 +176,25 @@ __global__ void __launch_bounds__(kThreads) census_kernel(const __grid_constant_
     uint64_t *o = out + (long long)img * out_stride;
     if (CW > 0 && x0 - CW / 2 >= 0 && x0 + kTileW + CW / 2 <= prm.W && y0 - CH / 2 >= 0 &&
         y0 + kTileH + CH / 2 <= prm.H) {
-        for (int k = threadIdx.x; k < kTileW * kTileH; k += kThreads) {
-            const int lx = k % kTileW, ly = k / kTileW;
-            o[(long long)(y0 + ly) * prm.W + x0 + lx] = census_px_in<(CW > 0 ? CW : 1), (CH > 0 ? CH : 1)>(tile, lx, ly);
+        if (SGM_CENSUS_SIMD && CW > 0 && CW <= 9) {
+            static_assert(kTileW * kTileH == 4 * kThreads, "one 4-pixel group per thread");
+            const int lx = 4 * (threadIdx.x % (kTileW / 4)), ly = threadIdx.x / (kTileW / 4);
+            uint64_t v[4];
+            census_px4_in<(CW > 0 && CW <= 9 ? CW : 1), (CH > 0 ? CH : 1)>(tile, lx, ly, v);
+            ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(o + (long long)(y0 + ly) * prm.W + x0 + lx);
+            if (((reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+                dst[0] = make_ulonglong2(v[0], v[1]);
+                dst[1] = make_ulonglong2(v[2], v[3]);
+            } else {
+                uint64_t *d1 = o + (long long)(y0 + ly) * prm.W + x0 + lx;
+                d1[0] = v[0]; d1[1] = v[1]; d1[2] = v[2]; d1[3] = v[3];
+            }
+        } else {
+            for (int k = threadIdx.x; k < kTileW * kTileH; k += kThreads) {
+                const int lx = k % kTileW, ly = k / kTileW;
+                o[(long long)(y0 + ly) * prm.W + x0 + lx] =
+                    census_px_in<(CW > 0 ? CW : 1), (CH > 0 ? CH : 1)>(tile, lx, ly);
+            }
         }
         return;
     }

@@ -291,6 +291,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
 
     // per-lane constants
     const uint32_t one = uint32_t(p.one);
+    const uint32_t k10001 = one * 0x10001u, kneg10001 = one * 0xFFFEFFFFu;   // (SGM_UR_MB)
     // the forward sweep takes the u16x2 constants as kernel-parameter operands (c[] bank:
     // forward sweep 21.38 -> 21.03 ms on 64 quads); the backward sweep computes them into
     // registers (as parameters it measured slower: 21.32 -> 21.46 ms, Wide 5.29 -> 5.87 ms)
@@ -564,14 +565,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
             uint32_t S[R];
             {
                 uint32_t nL[R];
-                path_update<R>(Lh, C, nL, negp1x2, p2mp1x2, twop1x2, sel_fold, ff_lane0);
+                path_update<R>(Lh, C, nL, negp1x2, p2mp1x2, twop1x2, sel_fold, ff_lane0, k10001, kneg10001);
 #pragma unroll
                 for (int r = 0; r < R; ++r) { Lh[r] = nL[r]; S[r] = nL[r]; }
             }
             uint32_t nv[3][R];
 #pragma unroll
             for (int v = 0; v < 3; ++v)
-                path_update<R>(pv[v], C, nv[v], negp1x2, p2mp1x2, twop1x2, sel_fold, ff_lane0);
+                path_update<R>(pv[v], C, nv[v], negp1x2, p2mp1x2, twop1x2, sel_fold, ff_lane0, k10001, kneg10001);
             // S = sum of the four unbiased path costs: the -4 P1 rides in IADD3's third slot
 #pragma unroll
             for (int r = 0; r < R; ++r) S[r] = (S[r] + nv[0][r] + nv[1][r]) + (nv[2][r] + negb4);

@@ -87,6 +87,10 @@ __device__ __forceinline__ void st_relaxed_gpu(int *p, int v) {
     asm volatile("st.relaxed.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
+#ifndef SGM_UR_MB
+#define SGM_UR_MB 0
+#endif
+
 // Integer multiply-add on the FMA pipe.  `one` is a runtime 1 (kernel parameter), so
 // ptxas cannot fold a*one+c into an ALU-pipe IADD3: the min-plus work saturates the
 // half-rate ALU pipe (VIMNMX / VIADDMNMX / PRMT / LOP3 all issue there), while IMAD
@@ -118,7 +122,8 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
 template <int R>
 __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uint32_t (&C)[R],
                                             uint32_t (&out)[R], uint32_t negp1x2, uint32_t p2mp1x2,
-                                            uint32_t twop1x2, uint32_t sel_fold, uint32_t ff_lane0) {
+                                            uint32_t twop1x2, uint32_t sel_fold, uint32_t ff_lane0,
+                                            uint32_t k10001 = 0x10001u, uint32_t kneg10001 = 0xFFFEFFFFu) {
     // mb = min_k Lb(p - r, k): min over the lane's pairs, then over the two halves (the
     // high half is brought down with IMAD.HI on the FMA pipe), then over the warp
     uint32_t v = prev[0];
@@ -126,8 +131,15 @@ __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uin
     for (int r = 1; r < R; ++r) v = __vminu2(v, prev[r]);
     v = __vminu2(v, __umulhi(v, 0x10000u));           // lo = min(lo, hi), hi = 0
     const uint32_t mb = __reduce_min_sync(0xffffffffu, v);
+#if SGM_UR_MB
+    // mb lives in a uniform register (CREDUX): as IMAD's B operand it needs no move to a
+    // vector register; the multipliers are runtime registers (k10001 = 0x10001, kneg = -0x10001)
+    const uint32_t mP2 = imad(k10001, mb, p2mp1x2);
+    const uint32_t K = imad(kneg10001, mb, twop1x2);
+#else
     const uint32_t mP2 = imad(mb, 0x10001u, p2mp1x2);  // m + P2 = mb - P1 + P2, both halves
     const uint32_t K = imad(mb, 0xFFFEFFFFu, twop1x2); // 2 P1 - mb in both halves (mod 2^32)
+#endif
     // neighbour pairs k-1 (of reg 0) and k+1 (of reg R-1)
     uint32_t up = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
     if (R > 2) up |= ff_lane0;
@@ -154,7 +166,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
 // Measured against a 20 us suspend hint (7.17 ms per step; the hinted form compiles to a
 // TRYWAIT + NANOSLEEP.SYNCS loop that woke ~70 times per wait) and a test_wait spin
 // (7.27 ms): the plain form is fastest (7.16 ms).
+#ifndef SGM_MBAR_HINT
+#define SGM_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+#if SGM_MBAR_HINT
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(b)),
+        "r"(parity), "n"(SGM_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n .reg .pred P1;\n"
         "WAIT_%=:\n"
@@ -162,6 +186,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
         " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(b)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // One mbarrier test (no retry loop): true once the phase with `parity` has completed.
