@@ -149,7 +149,11 @@ void band_geometry(int H, int nviews, int nsm, int *nbands, int *q, int *r) {
     if (forced >= sgm::kBandRowsMin && forced <= sgm::kBandRowsMax) {
         nb = bands(forced);
     } else if ((long long)nviews * bands(lo) >= 2LL * nsm) {
-        nb = waves(bands(hi)) < waves(bands(lo)) ? bands(hi) : bands(lo);
+        // hi rows only when that saves more than ~6 % of the waves: lo = 16 rows (4 compute
+        // warps per SM sub-partition) runs ~5 % more rows per second than 17 (64 quads: 42
+        // waves of 16 rows 43.67 ms vs 40 waves of 17 rows 43.89; 8 quads: 6 waves of 16 rows
+        // 6.21 ms vs 5 waves of 17 rows 5.99)
+        nb = 100 * waves(bands(hi)) < 94 * waves(bands(lo)) ? bands(hi) : bands(lo);
     } else {
         nb = bands(lo);
         double best = -1.0;
