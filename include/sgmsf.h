@@ -263,6 +263,13 @@ SGM_API sgm_status sgm_evaluate(sgm_handle *h, int32_t n, const float *sf, const
                         const uint8_t *gt_valid, const uint8_t *gt_noc, float tau_abs,
                         float tau_rel, uint64_t *counts, void *stream);
 
+/* KITTI rates from one [2][6] count block of sgm_evaluate (E3): for each
+ * split (0 = Occ, 1 = Noc) rates[split][0..3] = 100 * {n_d1, n_d2, n_fl, n_sf} / n_eval
+ * (percent of the evaluated pixels) and rates[split][4] = 100 * n_eval / n_gt (density,
+ * percent); a zero denominator gives NaN.  Host memory in and out (copy the device counts
+ * back first), no handle, no device work, thread-safe.  SGM_ERR_INVALID_ARGUMENT on NULL. */
+SGM_API sgm_status sgm_eval_rates(const uint64_t *counts, double *rates);
+
 /* ---- instrumentation ----------------------------------------------------- */
 enum { SGM_NUM_STAGES = 5 };   /* census, sweep_fwd, sweep_bwd_wta, lr_check, combine */
 

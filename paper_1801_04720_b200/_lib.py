@@ -25,7 +25,7 @@ EXPORTS = (
     "sgm_wta", "sgm_lr_check", "sgm_disparity", "sgm_combine_sceneflow", "sgm_scene_flow",
     "sgm_scene_flow_host", "sgm_set_timing", "sgm_read_timing", "sgm_stage_name",
     "sgm_launch_count", "sgm_get_geometry", "sgm_last_error_string", "sgm_debug_set_trace",
-    "sgm_evaluate", "sgm_scene_flow_stream", "sgm_scene_flow_stream_host",
+    "sgm_evaluate", "sgm_eval_rates", "sgm_scene_flow_stream", "sgm_scene_flow_stream_host",
     "sgm_get_device_error", "sgm_debug_set_flags",
     # include/sgmflow.h
     "sgm_flow_create", "sgm_flow_destroy", "sgm_flow_last_error_string", "sgm_flow_launch_count",
@@ -128,6 +128,7 @@ def load(path: str | None = None):
         "sgm_scene_flow_stream_host": (st, [P, I32, P, P, P, ctypes.POINTER(SgmCamera),
                                      ctypes.POINTER(SgmSceneflowOut), P]),
         "sgm_evaluate": (st, [P, I32, P, P, P, P, P, P, P, ctypes.c_float, ctypes.c_float, P, P]),
+        "sgm_eval_rates": (st, [ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_double)]),
         "sgm_set_timing": (st, [P, I32]),
         "sgm_read_timing": (I32, [P, ctypes.POINTER(ctypes.c_float)]),
         "sgm_stage_name": (ctypes.c_char_p, [I32]),

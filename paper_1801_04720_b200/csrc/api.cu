@@ -2,6 +2,7 @@
 // launch orchestration on the caller's stream, status codes, instrumentation.
 #include <cstdio>
 #include <cstdlib>
+#include <limits>
 #include <cstring>
 #include <new>
 
@@ -558,6 +559,19 @@ sgm_status sgm_evaluate(sgm_handle *h, int32_t n, const float *sf, const uint8_t
     cudaError_t e = sgm::launch_evaluate(p, static_cast<cudaStream_t>(stream));
     if (e == cudaSuccess) ++h->launches;
     return from_cuda(e);
+}
+
+sgm_status sgm_eval_rates(const uint64_t *counts, double *rates) {
+    if (!counts || !rates) return SGM_ERR_INVALID_ARGUMENT;
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    for (int split = 0; split < 2; ++split) {
+        const uint64_t *c = counts + 6 * split;
+        double *r = rates + 5 * split;
+        const uint64_t n_gt = c[0], n_ev = c[1];
+        for (int k = 0; k < 4; ++k) r[k] = n_ev ? 100.0 * double(c[2 + k]) / double(n_ev) : nan;
+        r[4] = n_gt ? 100.0 * double(n_ev) / double(n_gt) : nan;
+    }
+    return SGM_OK;
 }
 
 // 3D outputs need dp, valid_3d and a camera with f > 0, B > 0 (validated before any enqueue)

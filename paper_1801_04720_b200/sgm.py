@@ -260,16 +260,12 @@ class SGM:
 
 def rates_from_counts(counts):
     """{split: {D1, D2, Fl, SF (percent of evaluated pixels), density (percent)}} from
-    one [2][6] count block (host arithmetic on integers the kernel produced)."""
-    c = [[int(v) for v in row] for row in counts]
-    out = {}
-    for split, name in ((0, "occ"), (1, "noc")):
-        n_gt, n_ev = c[split][0], c[split][1]
-        r = {k: (100.0 * c[split][i] / n_ev if n_ev else float("nan"))
-             for k, i in (("D1", 2), ("D2", 3), ("Fl", 4), ("SF", 5))}
-        r["density"] = 100.0 * n_ev / n_gt if n_gt else float("nan")
-        out[name] = r
-    return out
+    one [2][6] count block, computed by the library (sgm_eval_rates)."""
+    c = (ctypes.c_uint64 * 12)(*[int(v) for row in counts for v in row])
+    r = (ctypes.c_double * 10)()
+    _lib.call("sgm_eval_rates", c, r)
+    return {name: dict(zip(("D1", "D2", "Fl", "SF", "density"), r[5 * split:5 * split + 5]))
+            for split, name in ((0, "occ"), (1, "noc"))}
 
 
 def stack_video(video, pitch, device):

@@ -133,3 +133,16 @@ def test_fault_and_debug_entry_points_reject_null():
     code = ctypes.c_int32(-1)
     assert lib.sgm_get_device_error(None, ctypes.byref(code), 0) == 1
     assert lib.sgm_debug_set_flags(None, 4) == 1
+
+
+def test_eval_rates_host_call():
+    """sgm_eval_rates (host arithmetic behind the boundary): hand-computed rates of one
+    [2][6] count block (SPEC S:479-481 style: 1 of 10 flow outliers -> Fl = SF = 10 %,
+    8 of 10 GT pixels evaluated -> density 80 %), and NaN for empty splits."""
+    import math
+    from paper_1801_04720_b200 import rates_from_counts
+    r = rates_from_counts([[10, 8, 2, 0, 1, 1], [0, 0, 0, 0, 0, 0]])
+    assert r["occ"] == {"D1": 25.0, "D2": 0.0, "Fl": 12.5, "SF": 12.5, "density": 80.0}
+    assert all(math.isnan(v) for v in r["noc"].values())
+    lib = _lib.load()
+    assert lib.sgm_eval_rates(None, None) != 0

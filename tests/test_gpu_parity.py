@@ -56,6 +56,12 @@ SHAPES = [
     (61, 23, 32, 7, 9, 7, 86),
     (61, 23, 32, 13, 3, 5, 60),
     (48, 21, 24, 3, 3, 0, 0),
+    # the band handoff in bytes (sweep_params h8): padded D at the clamp bound C_max + 2 P2 =
+    # 254, an odd width with 6 cells per lane (byte rows rounded up to an even position
+    # count), and P2 large enough (C_max + P2 + P1 > 255) to keep the u16 handoff
+    (200, 40, 96, 9, 7, 7, 96),
+    (261, 35, 192, 9, 7, 7, 86),
+    (200, 40, 128, 9, 7, 10, 190),
 ]
 
 
