@@ -90,6 +90,15 @@ struct CandW {
         const int b = int(__dp4a(t, wpack, 0u));
         return in ? abs(FQ2 * a - b) : pen64;
     }
+    // every sample of the (2r+1)^2 patch inside (the common case away from the borders):
+    // then no sample needs the bounds test or the penalty (same integers as cost())
+    __device__ __forceinline__ bool interior(int r) const {
+        return bx - r >= 0 && unsigned(bx + r) <= ux && by - r >= 0 && unsigned(by + r) <= uy;
+    }
+    __device__ __forceinline__ int cost_in(const uint32_t *__restrict__ QB, int soff, int a64) const {
+        const unsigned t = __ldg(QB + base + soff);
+        return abs(a64 - int(__dp4a(t, wpack, 0u)));
+    }
 };
 
 // The whole data term by one thread, sample order irrelevant (integers).  The
@@ -99,6 +108,23 @@ __device__ __forceinline__ int patch_cost_thread(const uint8_t *__restrict__ A, 
                                                  int W, int H, int x, int y, int fu, int fv, int r, int pen64) {
     const Cand c(fu, fv, W, H);
     int s = 0;
+    // the whole patch inside both images (the common case): no clamping, no bounds tests
+    if (x - r >= 0 && x + r < W && y - r >= 0 && y + r < H && x - r + c.qx >= 0 && x + r + c.qx <= c.ixmax &&
+        y - r + c.qy >= 0 && y + r + c.qy <= c.iymax) {
+        const uint8_t *arow = A + (y - r) * W + x;
+        const uint32_t *brow = QB + (y - r + c.qy) * W + x + c.qx;
+        for (int dy = -r; dy <= r; ++dy, arow += W, brow += W) {
+#pragma unroll
+            for (int k = 0; k < 15; ++k) {
+                const int dx = k - r;
+                if (dx <= r) {
+                    const int a = __ldg(arow + dx);
+                    s += abs(FQ2 * a - int(__dp4a(__ldg(brow + dx), c.wpack, 0u)));
+                }
+            }
+        }
+        return s;
+    }
     for (int dy = -r; dy <= r; ++dy) {
         const uint8_t *arow = A + clampi(y + dy, 0, H - 1) * W;
         const int iy = y + dy + c.qy;
@@ -490,12 +516,23 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
         if (eh && ev) {                             // both candidates: loads in flight together
             const CandW C0(hv.x, hv.y, x, y, W, H), C1(vv.x, vv.y, x, y, W, H);
             int s0 = 0, s1 = 0;
+            if (C0.interior(r) && C1.interior(r)) {     // (warp-uniform) no bounds tests
+#pragma unroll
+                for (int k = 0; k < NK; ++k) {
+                    const int a64 = FQ2 * a[k];
+                    const int t0 = C0.cost_in(dst, soff[k], a64);
+                    const int t1 = C1.cost_in(dst, soff[k], a64);
+                    s0 += sok[k] ? t0 : 0;
+                    s1 += sok[k] ? t1 : 0;
+                }
+            } else {
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
                 const int t0 = C0.cost(dst, sdx[k], sdy[k], soff[k], a[k], fs.pen64);
                 const int t1 = C1.cost(dst, sdx[k], sdy[k], soff[k], a[k], fs.pen64);
                 s0 += sok[k] ? t0 : 0;
                 s1 += sok[k] ? t1 : 0;
+            }
             }
             const int c0 = int(__reduce_add_sync(0xffffffffu, unsigned(s0)));
             const int c1 = int(__reduce_add_sync(0xffffffffu, unsigned(s1)));
@@ -505,10 +542,18 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
             const int2 w = eh ? hv : vv;
             const CandW C0(w.x, w.y, x, y, W, H);
             int s0 = 0;
+            if (C0.interior(r)) {
+#pragma unroll
+                for (int k = 0; k < NK; ++k) {
+                    const int t0 = C0.cost_in(dst, soff[k], FQ2 * a[k]);
+                    s0 += sok[k] ? t0 : 0;
+                }
+            } else {
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
                 const int t0 = C0.cost(dst, sdx[k], sdy[k], soff[k], a[k], fs.pen64);
                 s0 += sok[k] ? t0 : 0;
+            }
             }
             const int c0 = int(__reduce_add_sync(0xffffffffu, unsigned(s0)));
             if (c0 < cc) { cc = c0; cu = w.x; cv = w.y; }
