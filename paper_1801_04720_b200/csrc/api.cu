@@ -282,7 +282,7 @@ sgm_status sgm_create(const sgm_params *p, int32_t device, sgm_handle **out) {
     if (e == cudaSuccess) e = dalloc(&h->census, nv * npx);
     // the backward sweep prefetches S_fwd a few positions ahead without clamping: the
     // first row's prefetch reads into the front guard
-    constexpr size_t kSfwdGuard = 16;
+    constexpr size_t kSfwdGuard = 64;   // (covers the optional L2 prefetch distance too)
     if (e == cudaSuccess) e = dalloc(&h->sfwd_alloc, (nv * npx + kSfwdGuard) * size_t(h->dp));
     if (e == cudaSuccess) h->sfwd = h->sfwd_alloc + kSfwdGuard * size_t(h->dp);
     if (e == cudaSuccess) e = dalloc(&h->dint, nv * npx);

@@ -70,6 +70,24 @@
 #ifndef SGM_NAMED_LEAD
 #define SGM_NAMED_LEAD 0
 #endif
+// backward sweep: the sub-pixel / store block is only reachable at the last position of an
+// unrolled block when CPL divides 32 (1 = test it there only)
+#ifndef SGM_FIN_LAST
+#define SGM_FIN_LAST 0
+#endif
+// backward sweep: L2 prefetch of the S_fwd row this many positions ahead (0 = off)
+#ifndef SGM_L2PF
+#define SGM_L2PF 0
+#endif
+// backward sweep: S_fwd register prefetch depth (positions) for 6 / 8 cells per lane.
+// Measured (4 HighRes quads, CPL = 6): depth 2 9.75 ms, 3 10.32 ms, 6 9.44 ms (kept);
+// (8 Wide quads, CPL = 8): depth 2 5.29 ms (kept), 4 5.74 ms.  Outputs bit-identical.
+#ifndef SGM_PF6
+#define SGM_PF6 6
+#endif
+#ifndef SGM_PF8
+#define SGM_PF8 2
+#endif
 
 namespace sgm {
 namespace {
@@ -409,7 +427,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
     for (int k = 0; k < R; ++k) { lw[k] = 0; hw[k] = 0; }
     // BWD: S_fwd register prefetch PF positions ahead (slot = position mod PF must be a
     // compile-time index, so PF divides the unroll CPL)
-    constexpr int PF = (CPL == 4) ? 4 : 2;
+    constexpr int PF = (CPL == 4) ? 4 : (CPL == 6) ? SGM_PF6 : (CPL == 8) ? SGM_PF8 : 2;
+    static_assert(CPL % PF == 0, "the prefetch depth must divide the unrolled block");
     uint32_t pf[PF][R];
 #pragma unroll
     for (int k = 0; k < PF; ++k)
@@ -439,10 +458,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
 
 #if SGM_TAIL_SPLIT
     // one position of the row (ph = i mod CPL is a compile-time constant after unrolling)
-    auto position = [&](const int i0, const int ph) {
+    auto position = [&](const int i0, const int ph, const bool tail) {
         {
             const int i = i0 + ph;
 #else
+    constexpr bool tail = true;
 #pragma unroll 1
     for (int i0 = 0; i0 < W; i0 += CPL) {
 #pragma unroll
@@ -520,6 +540,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                 // result into the slot at once and stall on it.  Past the row's end it reads
                 // the row before (or the allocation's front guard); the value is never used.
                 VecIO<R>::ld(sfwd_ptr + PF * sstep, pf[slot]);
+#if SGM_L2PF
+                // once per block: lanes 0 .. (lines per block - 1) pull the block SGM_L2PF
+                // positions ahead into L2 (past the row's start it touches the row before or
+                // the front guard: harmless)
+                if (ph == 0) {
+                    constexpr int kLines = CPL * DP * 2 / 128;
+                    const char *a = reinterpret_cast<const char *>(sfwd_ptr - CPL * lane + SGM_L2PF * sstep) +
+                                    (BWD ? -128 * lane + (DP * 2 - 128) : 128 * lane);
+                    if (lane < kLines) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
+                }
+#endif
                 sfwd_ptr += sstep;
             } else {
                 const uint64_t rv = cref[i & 63];
@@ -691,7 +722,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                     if (lane == sl) { rec_key = bkey; rec_ac = sa | (sc << 16); }
                     // every 32 positions each lane finishes one pixel: the parabola
                     // sub-pixel (one IEEE division per lane) and the stores
-                    if (sl == 31 || i == W - 1) {
+                    // (whole blocks with CPL | 32: only their last position can be one)
+                    constexpr bool fin_last = SGM_FIN_LAST && SGM_TAIL_SPLIT && (32 % CPL == 0);
+                    if ((!fin_last || tail || ph == CPL - 1) && (sl == 31 || i == W - 1)) {
                         if (lane <= sl) {
                             const int d = int(rec_key & 0xffu);
                             const int b = int(rec_key >> 8);
@@ -720,12 +753,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
 #pragma unroll 1
     for (int i0 = 0; i0 < Wfull; i0 += CPL) {
 #pragma unroll
-        for (int ph = 0; ph < CPL; ++ph) position(i0, ph);
+        for (int ph = 0; ph < CPL; ++ph) position(i0, ph, false);
     }
     if (Wfull < W) {
 #pragma unroll
         for (int ph = 0; ph < CPL - 1; ++ph)
-            if (Wfull + ph < W) position(Wfull, ph);
+            if (Wfull + ph < W) position(Wfull, ph, true);
     }
 #endif
     if (has_row_below) {

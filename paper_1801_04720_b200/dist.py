@@ -122,3 +122,37 @@ def gather_results(out: dict, rank: int, world: int, device=None):
     recv = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
     gather_packed(buf, recv, rank, world)
     return recv
+
+
+class PipelinedGather:
+    """Gather of step k's packed results to rank 0, overlapped with step k+1's kernels.
+
+    submit(packed) copies the step's payload into a staging buffer on the current stream
+    and starts an asynchronous gather of it (NCCL runs it on its own stream, ordered after
+    the copy); the next step's kernels, which overwrite `packed`, are then free to run while
+    the payload travels.  The previous gather is awaited before the staging buffer is
+    reused, so at most one collective is in flight.  drain() waits for the last one; after
+    it rank 0's `recv[r]` holds rank r's payload of the most recent submit().
+    """
+
+    def __init__(self, packed: torch.Tensor, rank: int, world: int):
+        self.rank, self.world = rank, world
+        self.stage = torch.empty_like(packed)
+        self.recv = [torch.empty_like(packed) for _ in range(world)] if rank == 0 else None
+        self.work = None
+
+    def submit(self, packed: torch.Tensor):
+        self.drain()
+        self.stage.copy_(packed, non_blocking=True)
+        if self.world > 1:
+            if self.rank == 0:
+                self.work = dist.gather(self.stage, gather_list=self.recv, dst=0, async_op=True)
+            else:
+                self.work = dist.gather(self.stage, dst=0, async_op=True)
+        elif self.recv is not None:
+            self.recv[0].copy_(self.stage, non_blocking=True)
+
+    def drain(self):
+        if self.work is not None:
+            self.work.wait()
+            self.work = None

@@ -125,3 +125,61 @@ def test_gloo_world2_gather_and_max():
     assert res[0]["idx"] == [0, 1, 2] and res[1]["idx"] == [3, 4, 5]
     assert res[0]["tmax"] == 20.0 and res[1]["tmax"] == 20.0
     assert res[0]["frames"] == [0, 1, 2, 3, 4, 5]
+
+
+def _pipe_worker(rank, world, port, q):
+    """Three pipelined steps: the payload of step k is overwritten (as the next step's
+    kernels would) right after submit(); rank 0 must still receive step k's bytes."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        n, H, W = 2, 2, 3
+        packed = torch.empty(sd.packed_bytes(n, H, W), dtype=torch.uint8)
+        pipe = sd.PipelinedGather(packed, rank, world)
+        seen = []
+        for step in range(3):
+            packed.fill_(10 * step + rank + 1)           # "compute" step k
+            pipe.submit(packed)
+            packed.fill_(255)                            # step k+1 starts overwriting
+            if step == 1:                                # a reader between steps
+                pipe.drain()
+                if rank == 0:
+                    seen.append([int(b[0]) for b in pipe.recv] + [int(b[-1]) for b in pipe.recv])
+        pipe.drain()
+        assert pipe.work is None
+        if rank == 0:
+            seen.append([int(b[0]) for b in pipe.recv] + [int(b[-1]) for b in pipe.recv])
+            for b in pipe.recv:
+                assert bool((b == b[0]).all())
+        dist.destroy_process_group()
+        q.put({"rank": rank, "seen": seen})
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        q.put({"rank": rank, "error": repr(e)})
+
+
+def test_gloo_world2_pipelined_gather():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipe_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    res = {r["rank"]: r for r in res}
+    for r in res.values():
+        assert "error" not in r, r
+    # after step 1: payloads 11 (rank 0) and 12 (rank 1); after step 2: 21 and 22
+    assert res[0]["seen"] == [[11, 12, 11, 12], [21, 22, 21, 22]]
+
+
+def test_pipelined_gather_single_rank():
+    packed = torch.arange(34 * 6, dtype=torch.uint8)
+    pipe = sd.PipelinedGather(packed, 0, 1)
+    pipe.submit(packed)
+    packed.zero_()
+    pipe.drain()
+    assert torch.equal(pipe.recv[0], torch.arange(34 * 6, dtype=torch.uint8))
