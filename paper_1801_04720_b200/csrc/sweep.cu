@@ -70,20 +70,44 @@
 #ifndef SGM_NAMED_LEAD
 #define SGM_NAMED_LEAD 0
 #endif
-// backward sweep: the sub-pixel / store block is only reachable at the last position of an
-// unrolled block when CPL divides 32 (1 = test it there only)
+// backward sweep: the sub-pixel / store block (one pixel per lane, every kWtaPeriod positions)
+// is only reachable at the last position of an unrolled block when CPL divides the period:
+// 1 = test for it there only.  Without it every position carried a BSSY / BRA / BSYNC region
+// that also fenced the scheduler: 8 Driving quads backward sweep 2.912 -> 2.714 ms, 64 quads
+// 21.19 -> 19.63 ms, 8 Wide quads 5.28 -> 5.06 ms (bit-identical).  For 6 cells per lane the
+// period is 30 positions (SGM_PER30; lanes 30, 31 hold no pixel).
 #ifndef SGM_FIN_LAST
-#define SGM_FIN_LAST 0
+#define SGM_FIN_LAST 1
 #endif
-// backward sweep: L2 prefetch of the S_fwd row this many positions ahead (0 = off)
-#ifndef SGM_L2PF
-#define SGM_L2PF 0
+// band input (gbuf rows of the band above): L2 prefetch this many positions ahead (0 = off)
+#ifndef SGM_GIN_L2PF
+#define SGM_GIN_L2PF 0
+#endif
+#ifndef SGM_REFILL_FIRST
+#define SGM_REFILL_FIRST 0
+#endif
+#ifndef SGM_PER30
+#define SGM_PER30 1
+#endif
+// backward sweep: L2 prefetch of the S_fwd row this many positions ahead, per cells-per-lane
+// (0 = off).  Measured with SGM_FIN_LAST: 8 Wide quads (CPL 8) 5.06 -> 4.44 ms with 16; 4
+// HighRes quads (CPL 6) 9.75 -> 9.33 ms with 16 (32: 9.42); 8 Driving quads (CPL 4) 2.714 ->
+// 2.775 ms with 16 (off).
+#ifndef SGM_L2PF4
+#define SGM_L2PF4 0
+#endif
+#ifndef SGM_L2PF6
+#define SGM_L2PF6 16
+#endif
+#ifndef SGM_L2PF8
+#define SGM_L2PF8 16
 #endif
 // backward sweep: S_fwd register prefetch depth (positions) for 6 / 8 cells per lane.
-// Measured (4 HighRes quads, CPL = 6): depth 2 9.75 ms, 3 10.32 ms, 6 9.44 ms (kept);
-// (8 Wide quads, CPL = 8): depth 2 5.29 ms (kept), 4 5.74 ms.  Outputs bit-identical.
+// Measured, 4 HighRes quads (CPL = 6) before the L2 prefetch: depth 2 9.75 ms, 3 10.32 ms, 6
+// 9.44 ms; with the L2 prefetch and the 30-position WTA period: depth 2 8.80 ms (kept), 6 8.92
+// ms.  8 Wide quads (CPL = 8): depth 2 4.45 ms (kept), 4 4.49 ms.  Outputs bit-identical.
 #ifndef SGM_PF6
-#define SGM_PF6 6
+#define SGM_PF6 2
 #endif
 #ifndef SGM_PF8
 #define SGM_PF8 2
@@ -439,7 +463,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
         for (int k = 0; k < PF; ++k)
             if (k < W) VecIO<R>::ld(sfwd_ptr + k * sstep, pf[k]);
     }
-    uint32_t rec_key = 0, rec_ac = 0;                // BWD: WTA record of position (i & ~31) + lane
+    // BWD: WTA record of position (i - i mod kWtaPeriod) + lane, finished every kWtaPeriod positions
+    constexpr int kWtaPeriod = (SGM_PER30 && SGM_TAIL_SPLIT && CPL == 6) ? 30 : 32;
+    int pbase = 0;                                   // i0 mod kWtaPeriod (kWtaPeriod != 32 only)
+    uint32_t rec_key = 0, rec_ac = 0;
     constexpr bool do_wta = BWD && !SOUT;
     constexpr bool do_sout = BWD && SOUT;
     int16_t *dint_row = do_wta ? p.dint + (long long)view * p.disp_view_stride + yrow : nullptr;
@@ -473,6 +500,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
             const int xv = xview(i);
             // --- inputs of the row above
             if (band_input) {
+                if (SGM_GIN_L2PF > 0 && ph == 0 && i + SGM_GIN_L2PF + CPL <= W) {
+                    // the band above finished these handoff rows long ago (band-major tickets)
+                    // and at large batches they have left L2: pull them back ahead of the
+                    // cp.async that needs them
+                    constexpr int kL = CPL * VEC * 2 / 128;
+                    const char *a = reinterpret_cast<const char *>(gin + (long long)(i + SGM_GIN_L2PF) * VEC);
+#pragma unroll
+                    for (int c = 0; c < kL; c += 32)
+                        if (c + lane < kL) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a + 128 * (c + lane)));
+                }
                 if ((ph % G) == 0) {                   // group start: keep LG groups in flight
                     issue_input(i / G + LG);
                     cp_async_wait<LG>();
@@ -489,9 +526,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                 }
                 else mbar_wait(src_full + (g % RG), unsigned(g / RG) & 1u);
             }
-            // --- census prefetch refill
+            // --- census prefetch refill (i0 is a multiple of CPL: with CPL | 16 only the first
+            // position of a block can be a refill point)
+            constexpr bool rf_first = SGM_REFILL_FIRST && (16 % CPL == 0);
             if (BWD) {
-            } else if ((i & 31) == 0) {
+            } else if ((!rf_first || ph == 0) && (i & 31) == 0) {
                 const int q = min(i + 32 + lane, W - 1);   // clamped: keeps the loads unpredicated
                 {
                     const int xq = xview(q);
@@ -500,7 +539,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                     stage_ref = __ldg(ref_row + X(xq));
                     stage_fresh = __ldg(match_row + X(xm));
                 }
-            } else if ((i & 31) == 16) {
+            } else if ((!rf_first || ph == 0) && (i & 31) == 16) {
                 const int q = i + 16 + lane;
                 if (q < W) {
                     cref[q & 63] = stage_ref;
@@ -540,17 +579,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                 // result into the slot at once and stall on it.  Past the row's end it reads
                 // the row before (or the allocation's front guard); the value is never used.
                 VecIO<R>::ld(sfwd_ptr + PF * sstep, pf[slot]);
-#if SGM_L2PF
+                constexpr int L2PF = (CPL == 4) ? SGM_L2PF4 : (CPL == 6) ? SGM_L2PF6 : (CPL == 8) ? SGM_L2PF8 : 0;
                 // once per block: lanes 0 .. (lines per block - 1) pull the block SGM_L2PF
                 // positions ahead into L2 (past the row's start it touches the row before or
                 // the front guard: harmless)
-                if (ph == 0) {
+                if (L2PF > 0 && ph == 0) {
                     constexpr int kLines = CPL * DP * 2 / 128;
-                    const char *a = reinterpret_cast<const char *>(sfwd_ptr - CPL * lane + SGM_L2PF * sstep) +
+                    const char *a = reinterpret_cast<const char *>(sfwd_ptr - CPL * lane + L2PF * sstep) +
                                     (BWD ? -128 * lane + (DP * 2 - 128) : 128 * lane);
                     if (lane < kLines) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
                 }
-#endif
                 sfwd_ptr += sstep;
             } else {
                 const uint64_t rv = cref[i & 63];
@@ -718,13 +756,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                     const uint32_t sa = wta[dstar + 1];
                     const uint32_t sc = wta[dstar + 3];
 #endif
-                    const int sl = i & 31;
+                    // WTA record slot of this position: i mod kWtaPeriod (pbase = i0 mod period)
+                    const int sl = (kWtaPeriod == 32) ? (i & 31) : pbase + ph;
                     if (lane == sl) { rec_key = bkey; rec_ac = sa | (sc << 16); }
                     // every 32 positions each lane finishes one pixel: the parabola
                     // sub-pixel (one IEEE division per lane) and the stores
                     // (whole blocks with CPL | 32: only their last position can be one)
-                    constexpr bool fin_last = SGM_FIN_LAST && SGM_TAIL_SPLIT && (32 % CPL == 0);
-                    if ((!fin_last || tail || ph == CPL - 1) && (sl == 31 || i == W - 1)) {
+                    constexpr bool fin_last = SGM_FIN_LAST && SGM_TAIL_SPLIT && (kWtaPeriod % CPL == 0);
+                    if ((!fin_last || tail || ph == CPL - 1) && (sl == kWtaPeriod - 1 || i == W - 1)) {
                         if (lane <= sl) {
                             const int d = int(rec_key & 0xffu);
                             const int b = int(rec_key >> 8);
@@ -737,7 +776,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                                 off = fminf(fmaxf(off, -0.5f), 0.5f);
                                 sub = __fadd_rn(float(d), off);
                             }
-                            const int xo = X(xview((i & ~31) + lane));
+                            const int xo = X(xview((i - sl) + lane));
                             dint_row[xo] = int16_t(d);
                             dsub_row[xo] = sub;
                         }
@@ -754,6 +793,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
     for (int i0 = 0; i0 < Wfull; i0 += CPL) {
 #pragma unroll
         for (int ph = 0; ph < CPL; ++ph) position(i0, ph, false);
+        if (BWD && kWtaPeriod != 32) pbase = (pbase + CPL == kWtaPeriod) ? 0 : pbase + CPL;
     }
     if (Wfull < W) {
 #pragma unroll
