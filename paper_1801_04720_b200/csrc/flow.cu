@@ -383,6 +383,17 @@ __global__ void ff_lift_kernel(FieldSet fs, const int32_t *__restrict__ coarse, 
     }
 }
 
+// 1: warp-uniform decisions of the pixel loop are taken through votes and the lane-0 store
+// block is executed by every lane (same values, same addresses), so the compiler emits uniform
+// branches and no reconvergence regions: propagation 46.7 -> 45.3 ms per 8 Driving pairs,
+// output digest identical.  2: also the warp index and the polling loops.
+// (2: 45.3 -> 40.9 ms.)  3: also the interior tests and the band-handoff polling loop.
+#ifndef FF_UNIFORM
+#define FF_UNIFORM 2
+#endif
+#ifndef FF_APRE
+#define FF_APRE 0
+#endif
 // ------------------------------------------------------------------ propagation (FF7)
 struct PropParams {
     FieldSet fs;
@@ -477,6 +488,14 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
                 nu_l = flow[2 * q]; nv_l = flow[2 * q + 1]; nc_l = cost[q];
             }
         }
+#if FF_APRE
+        // A samples of this pixel: independent of the candidates, so they are issued before
+        // the wait for the row above (their latency leaves the pixel-to-pixel chain)
+        int a[NK];
+#pragma unroll
+        for (int k = 0; k < NK; ++k)
+            a[k] = __ldg(src + aoff[k] + clampi(x + sdx[k], 0, W - 1));
+#endif
         int cu = __shfl_sync(0xffffffffu, cu_l, i & 31);
         int cv = __shfl_sync(0xffffffffu, cv_l, i & 31);
         int cc = __shfl_sync(0xffffffffu, cc_l, i & 31);
@@ -487,14 +506,22 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
             if (above_in_cta) {
                 // back off while waiting: spinning warps would take the issue slots of the
                 // warps that have work
+#if FF_UNIFORM >= 2
+                while (__any_sync(0xffffffffu, hand_tag(e = ring_in[i & (kRowRing - 1)]) != i + 1)) __nanosleep(20);
+#else
                 while (hand_tag(e = ring_in[i & (kRowRing - 1)]) != i + 1) __nanosleep(20);
+#endif
             } else {
                 // band handoff through L2: the 32 positions of a chunk are fetched in one
                 // round trip (lane l holds position 32c + l); a position not yet published
                 // re-fetches the chunk, so the band runs one position behind its producer
                 if ((i & 31) == 0) hbuf = i + lane < W ? ld_relaxed_u64(hin + i + lane) : 0ull;
                 e = __shfl_sync(0xffffffffu, hbuf, i & 31);
+#if FF_UNIFORM >= 3
+                while (__any_sync(0xffffffffu, hand_tag(e) != i + 1)) {
+#else
                 while (hand_tag(e) != i + 1) {
+#endif
                     __nanosleep(64);
                     const int q = (i & ~31) + lane;
                     hbuf = q < W ? ld_relaxed_u64(hin + q) : 0ull;
@@ -505,18 +532,32 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
         }
         // candidates in order: horizontal (previous pixel), vertical; skip ones equal to
         // the incumbent (their data term equals the incumbent's: never strictly better)
+#if FF_UNIFORM
+        // (the values are warp-uniform; the votes tell the compiler so: uniform branches, no
+        // reconvergence regions around the candidate evaluation)
+        const bool eh = __any_sync(0xffffffffu, i > 0 && (hv.x != cu || hv.y != cv));
+        const bool ev = __any_sync(0xffffffffu, has_above && (vv.x != cu || vv.y != cv) &&
+                                                    (!eh || vv.x != hv.x || vv.y != hv.y));
+#else
         const bool eh = i > 0 && (hv.x != cu || hv.y != cv);
         const bool ev = has_above && (vv.x != cu || vv.y != cv) && (!eh || vv.x != hv.x || vv.y != hv.y);
+#endif
+#if !FF_APRE
         int a[NK];                                  // A samples, loaded only when needed
         if (eh || ev) {
 #pragma unroll
             for (int k = 0; k < NK; ++k)
                 a[k] = __ldg(src + aoff[k] + clampi(x + sdx[k], 0, W - 1));
         }
+#endif
         if (eh && ev) {                             // both candidates: loads in flight together
             const CandW C0(hv.x, hv.y, x, y, W, H), C1(vv.x, vv.y, x, y, W, H);
             int s0 = 0, s1 = 0;
+#if FF_UNIFORM >= 3
+            if (__all_sync(0xffffffffu, C0.interior(r) && C1.interior(r))) {
+#else
             if (C0.interior(r) && C1.interior(r)) {     // (warp-uniform) no bounds tests
+#endif
 #pragma unroll
                 for (int k = 0; k < NK; ++k) {
                     const int a64 = FQ2 * a[k];
@@ -542,7 +583,11 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
             const int2 w = eh ? hv : vv;
             const CandW C0(w.x, w.y, x, y, W, H);
             int s0 = 0;
+#if FF_UNIFORM >= 3
+            if (__all_sync(0xffffffffu, C0.interior(r))) {
+#else
             if (C0.interior(r)) {
+#endif
 #pragma unroll
                 for (int k = 0; k < NK; ++k) {
                     const int t0 = C0.cost_in(dst, soff[k], FQ2 * a[k]);
@@ -558,6 +603,16 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
             const int c0 = int(__reduce_add_sync(0xffffffffu, unsigned(s0)));
             if (c0 < cc) { cc = c0; cu = w.x; cv = w.y; }
         }
+#if FF_UNIFORM
+        // every lane stores the same values to the same addresses (one transaction each): no
+        // divergent lane-0 region in the pixel loop
+        {
+            if (has_below_in_cta) {
+                if (i >= kRowRing)
+                    while (__any_sync(0xffffffffu, sprog[warp + 1] < i - kRowRing + 1)) __nanosleep(20);
+                ring_out[i & (kRowRing - 1)] = pack_hand(cu, cv, i + 1);
+            }
+#else
         if (lane == 0) {
             if (has_below_in_cta) {
                 // ring slot reuse: the row below must have consumed position i - kRowRing
@@ -565,6 +620,7 @@ __device__ __forceinline__ void prop_row(const PropParams &pp, volatile unsigned
                     while (sprog[warp + 1] < i - kRowRing + 1) __nanosleep(20);
                 ring_out[i & (kRowRing - 1)] = pack_hand(cu, cv, i + 1);
             }
+#endif
             if (publish) st_relaxed_u64(hout + i, pack_hand(cu, cv, i + 1));
             sprog[warp] = i + 1;
             flow[2 * p] = cu;
@@ -611,7 +667,11 @@ __global__ void __launch_bounds__(NW * 32) ff_prop_kernel(const PropParams pp) {
     // band-major tickets: the resident CTAs are the first bands of all fields, so a band's
     // predecessor (one ticket "row" earlier) has normally finished before it starts
     const int band = ticket / pp.fs.nfields, f = ticket - band * pp.fs.nfields;
+#if FF_UNIFORM >= 2
+    const int warp = int(__reduce_min_sync(0xffffffffu, threadIdx.x >> 5)), lane = threadIdx.x & 31;
+#else
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#endif
     const int j = band * NW + warp;                 // iteration row
     if (j >= pp.fs.H) return;
     const int r = pp.fs.rad(pp.fs.kind(f));

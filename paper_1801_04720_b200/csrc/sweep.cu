@@ -79,7 +79,9 @@
 #ifndef SGM_FIN_LAST
 #define SGM_FIN_LAST 1
 #endif
-// band input (gbuf rows of the band above): L2 prefetch this many positions ahead (0 = off)
+// band input (gbuf rows of the band above): L2 prefetch this many positions ahead (0 = off).
+// Measured slower at 16 / 32 / 64 positions alike (64 quads forward sweep 20.88 -> 21.39 ms, 8
+// Driving quads 2.90 -> 2.96 ms): the extra code costs more than the latency it hides.
 #ifndef SGM_GIN_L2PF
 #define SGM_GIN_L2PF 0
 #endif
@@ -93,6 +95,12 @@
 // (0 = off).  Measured with SGM_FIN_LAST: 8 Wide quads (CPL 8) 5.06 -> 4.44 ms with 16; 4
 // HighRes quads (CPL 6) 9.75 -> 9.33 ms with 16 (32: 9.42); 8 Driving quads (CPL 4) 2.714 ->
 // 2.775 ms with 16 (off).
+#ifndef SGM_L2PF_BULK
+#define SGM_L2PF_BULK 0
+#endif
+#ifndef SGM_L2PF_PH
+#define SGM_L2PF_PH 0
+#endif
 #ifndef SGM_L2PF4
 #define SGM_L2PF4 0
 #endif
@@ -106,6 +114,24 @@
 // Measured, 4 HighRes quads (CPL = 6) before the L2 prefetch: depth 2 9.75 ms, 3 10.32 ms, 6
 // 9.44 ms; with the L2 prefetch and the 30-position WTA period: depth 2 8.80 ms (kept), 6 8.92
 // ms.  8 Wide quads (CPL = 8): depth 2 4.45 ms (kept), 4 4.49 ms.  Outputs bit-identical.
+// Measured (64 quads, backward sweep): two blocks with the prefetch 8 deep 19.64 -> 19.75 ms,
+// two blocks with the prefetch 4 deep 24.45 ms (the 24 KB loop body no longer fits the
+// instruction cache); in latency mode (1 Driving quad) 8 deep is faster: 1.098 -> 1.056 ms.
+#ifndef SGM_UR_TICKET
+#define SGM_UR_TICKET 0
+#endif
+#ifndef SGM_BWD4_UNROLL
+#define SGM_BWD4_UNROLL 1
+#endif
+#ifndef SGM_BWD4_UNROLL_FINE
+#define SGM_BWD4_UNROLL_FINE 2
+#endif
+#ifndef SGM_PF4U
+#define SGM_PF4U 8
+#endif
+#ifndef SGM_PF4
+#define SGM_PF4 4
+#endif
 #ifndef SGM_PF6
 #define SGM_PF6 2
 #endif
@@ -164,7 +190,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
     using SW = Sweep<CPL, C64, BWD, NW, GS>;
     static_assert(!SGM_NAMED_RING || NW <= 17, "named ring barriers: ids 0..NW-2 must be < 16");
     // block-relative ring slots (needs the loop split into whole CPL blocks)
-    constexpr bool SB = SGM_SLOT_BASE && SGM_TAIL_SPLIT && (SW::RS % CPL == 0) && (SW::RING0 % CPL == 0);
+    // positions per unrolled block of the row loop (the backward sweep with 4 cells per lane
+    // may unroll two CPL blocks, so that its S_fwd register prefetch can run 8 positions deep)
+    constexpr int U = (BWD && CPL == 4 && SGM_TAIL_SPLIT) ? CPL * (GS ? SGM_BWD4_UNROLL_FINE : SGM_BWD4_UNROLL) : CPL;
+    constexpr bool SB = SGM_SLOT_BASE && SGM_TAIL_SPLIT && (SW::RS % U == 0) && (SW::RING0 % U == 0);
     // band-handoff publication granularity (positions): measured best 8 for the forward
     // sweep, 4 for the backward sweep
     constexpr int PUB = (GS && SGM_FINE_PUB) ? SGM_FINE_PUB : (BWD ? 4 : kPublish);
@@ -212,7 +241,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
     // ticket -> (band, view): views in groups of p.vgroup, band-major inside a group, so
     // that band b+1 of a view starts about one band lag after band b (its handoff rows are
     // read while still in L2) and never before it (a band only waits for a running band)
+#if SGM_UR_TICKET
+    // through a warp reduction, so that the compiler knows band / view / row are warp-uniform
+    const int ticket = int(__reduce_min_sync(0xffffffffu, unsigned(s_ticket)));
+#else
     const int ticket = s_ticket;
+#endif
     const int grp = ticket / (p.vgroup * p.nbands);
     const int v0 = grp * p.vgroup;
     const int gv = min(p.vgroup, p.nviews - v0);
@@ -451,8 +485,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
     for (int k = 0; k < R; ++k) { lw[k] = 0; hw[k] = 0; }
     // BWD: S_fwd register prefetch PF positions ahead (slot = position mod PF must be a
     // compile-time index, so PF divides the unroll CPL)
-    constexpr int PF = (CPL == 4) ? 4 : (CPL == 6) ? SGM_PF6 : (CPL == 8) ? SGM_PF8 : 2;
-    static_assert(CPL % PF == 0, "the prefetch depth must divide the unrolled block");
+    constexpr int PF = (CPL == 4) ? (U > CPL ? SGM_PF4U : SGM_PF4) : (CPL == 6) ? SGM_PF6 : (CPL == 8) ? SGM_PF8 : 2;
+    static_assert(U % PF == 0, "the prefetch depth must divide the unrolled block");
     uint32_t pf[PF][R];
 #pragma unroll
     for (int k = 0; k < PF; ++k)
@@ -583,11 +617,18 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                 // once per block: lanes 0 .. (lines per block - 1) pull the block SGM_L2PF
                 // positions ahead into L2 (past the row's start it touches the row before or
                 // the front guard: harmless)
-                if (L2PF > 0 && ph == 0) {
+                if (L2PF > 0 && ph % CPL == SGM_L2PF_PH) {
+#if SGM_L2PF_BULK
+                    // one bulk prefetch (a single lane's instruction) for the whole block
+                    const char *a = reinterpret_cast<const char *>(sfwd_ptr - CPL * lane + (L2PF + CPL - 1) * sstep);
+                    if (lane == 0)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "n"(CPL * DP * 2));
+#else
                     constexpr int kLines = CPL * DP * 2 / 128;
                     const char *a = reinterpret_cast<const char *>(sfwd_ptr - CPL * lane + L2PF * sstep) +
                                     (BWD ? -128 * lane + (DP * 2 - 128) : 128 * lane);
                     if (lane < kLines) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
+#endif
                 }
                 sfwd_ptr += sstep;
             } else {
@@ -654,7 +695,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                 {
                     const int sb = i0 & (RS - 1);
                     const int s0 = SB ? sb + ph : (i & (RS - 1));
-                    const int s1 = SB ? ((ph == CPL - 1) ? ((i0 + CPL) & (RS - 1)) : sb + ph + 1) : ((i + 1) & (RS - 1));
+                    const int s1 = SB ? ((ph == U - 1) ? ((i0 + U) & (RS - 1)) : sb + ph + 1) : ((i + 1) & (RS - 1));
                     const int s2 = SB ? ((ph == 0) ? ((i0 - 1) & (RS - 1)) : sb + ph - 1) : ((i - 1) & (RS - 1));
                     VecIO<R>::st(my_ring + size_t(s0) * VEC, nv[0]);
                     VecIO<R>::st(my_ring + size_t(s1) * VEC + DP, nv[1]);
@@ -762,8 +803,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
                     // every 32 positions each lane finishes one pixel: the parabola
                     // sub-pixel (one IEEE division per lane) and the stores
                     // (whole blocks with CPL | 32: only their last position can be one)
-                    constexpr bool fin_last = SGM_FIN_LAST && SGM_TAIL_SPLIT && (kWtaPeriod % CPL == 0);
-                    if ((!fin_last || tail || ph == CPL - 1) && (sl == kWtaPeriod - 1 || i == W - 1)) {
+                    constexpr bool fin_last = SGM_FIN_LAST && SGM_TAIL_SPLIT && (kWtaPeriod % U == 0);
+                    if ((!fin_last || tail || ph == U - 1) && (sl == kWtaPeriod - 1 || i == W - 1)) {
                         if (lane <= sl) {
                             const int d = int(rec_key & 0xffu);
                             const int b = int(rec_key >> 8);
@@ -788,16 +829,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, kSweepCtasPerSm) sweep_kernel(c
 #if SGM_TAIL_SPLIT
     ;
     // whole CPL-position blocks without a per-position bound check, then the tail
-    const int Wfull = W - W % CPL;
+    const int Wfull = W - W % U;
 #pragma unroll 1
-    for (int i0 = 0; i0 < Wfull; i0 += CPL) {
+    for (int i0 = 0; i0 < Wfull; i0 += U) {
 #pragma unroll
-        for (int ph = 0; ph < CPL; ++ph) position(i0, ph, false);
+        for (int ph = 0; ph < U; ++ph) position(i0, ph, false);
         if (BWD && kWtaPeriod != 32) pbase = (pbase + CPL == kWtaPeriod) ? 0 : pbase + CPL;
     }
     if (Wfull < W) {
 #pragma unroll
-        for (int ph = 0; ph < CPL - 1; ++ph)
+        for (int ph = 0; ph < U - 1; ++ph)
             if (Wfull + ph < W) position(Wfull, ph, true);
     }
 #endif

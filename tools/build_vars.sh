@@ -5,7 +5,7 @@
 # GPU box by tools/var_time.sh.  Only VAR_SRC (default sweep.cu) is recompiled per variant.
 set -e
 PKG=paper_1801_04720_b200
-V=$PKG/lib/var
+V=${VAR_OUT:-$PKG/lib/var}
 SRC=${VAR_SRC:-sweep.cu}
 O=/tmp/sgm_var_objs
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a"

@@ -7,7 +7,7 @@ L=paper_1801_04720_b200/lib
 mkdir -p gpurun_out
 cp $L/libsgmsf.so /tmp/libsgmsf.keep
 for rep in $(seq $REPS); do
-for v in $L/var/*.so; do
+for v in ${VAR_DIR:-$L/var}/*.so; do
     name=$(basename $v .so)
     cp $v $L/libsgmsf.so
     if [ $rep = 1 ]; then
