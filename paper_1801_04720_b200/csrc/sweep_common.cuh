@@ -131,7 +131,12 @@ __device__ __forceinline__ void path_update(const uint32_t (&prev)[R], const uin
     for (int r = 1; r < R; ++r) v = __vminu2(v, prev[r]);
     v = __vminu2(v, __umulhi(v, 0x10000u));           // lo = min(lo, hi), hi = 0
     const uint32_t mb = __reduce_min_sync(0xffffffffu, v);
-#if SGM_UR_MB
+#if SGM_UR_MB == 2
+    // plain expressions: the compiler may keep both in the uniform datapath (mb is the
+    // CREDUX result in a uniform register, the constants are uniform)
+    const uint32_t mP2 = mb * 0x10001u + p2mp1x2;
+    const uint32_t K = twop1x2 - mb * 0x10001u;
+#elif SGM_UR_MB
     // mb lives in a uniform register (CREDUX): as IMAD's B operand it needs no move to a
     // vector register; the multipliers are runtime registers (k10001 = 0x10001, kneg = -0x10001)
     const uint32_t mP2 = imad(k10001, mb, p2mp1x2);
