@@ -23,7 +23,9 @@ def init_distributed(world: int, rank: int):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29533")
     os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
-    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    # SGM_DIST_BACKEND=gloo: functional runs of the multi-rank code on one GPU (two NCCL
+    # ranks cannot share a device); device payloads are then staged through the host
+    backend = os.environ.get("SGM_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
     kw = {}
     if backend == "nccl":
         kw["device_id"] = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
@@ -105,6 +107,14 @@ def gather_packed(buf: torch.Tensor, recv, rank: int, world: int):
     collective; NCCL with device tensors, gloo with host tensors)."""
     if world <= 1:
         return
+    if buf.is_cuda and dist.get_backend() != "nccl":       # gloo: stage through the host
+        host = buf.cpu()
+        hrecv = [torch.empty_like(host) for _ in range(world)] if rank == 0 else None
+        gather_packed(host, hrecv, rank, world)
+        if rank == 0:
+            for d, h in zip(recv, hrecv):
+                d.copy_(h)
+        return
     if rank == 0:
         dist.gather(buf, gather_list=recv, dst=0)
     else:
@@ -144,7 +154,9 @@ class PipelinedGather:
     def submit(self, packed: torch.Tensor):
         self.drain()
         self.stage.copy_(packed, non_blocking=True)
-        if self.world > 1:
+        if self.world > 1 and self.stage.is_cuda and dist.get_backend() != "nccl":
+            gather_packed(self.stage, self.recv, self.rank, self.world)   # gloo: synchronous
+        elif self.world > 1:
             if self.rank == 0:
                 self.work = dist.gather(self.stage, gather_list=self.recv, dst=0, async_op=True)
             else:
@@ -156,3 +168,75 @@ class PipelinedGather:
         if self.work is not None:
             self.work.wait()
             self.work = None
+
+
+class DirectGather:
+    """Zero-copy gather over peer memory: rank 0 owns `slots` buffers of world x nbytes; every
+    other rank maps them through CUDA IPC (peer access: NVLink / NVSwitch on a multi-GPU box)
+    and hands its slice to sgm_scene_flow as the output buffer, so the combination kernel's
+    own stores carry the payload to rank 0 -- no collective, no staging copy.  Rank 0 may
+    read slot s once `fence()` of the step that wrote it has returned on every rank (one
+    tiny all-reduce ordered after the step on the current stream).
+
+    Only torch plumbing is used (torch.multiprocessing's CUDA IPC handles, sent with
+    broadcast_object_list); construction is collective and either succeeds on every rank or
+    raises on every rank (`ok` is agreed with an all-reduce).
+    """
+
+    def __init__(self, nbytes: int, rank: int, world: int, device, slots: int = 2):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.rank, self.world, self.nbytes = rank, world, nbytes
+        # slices start 256-byte aligned (the kernels store float4)
+        self.stride = stride = (nbytes + 255) // 256 * 256
+        self.device = torch.device(device)
+        self.bufs, err = None, None
+        obj = [None]
+        try:
+            if rank == 0:
+                self.bufs = [torch.empty(world * stride, dtype=torch.uint8, device=self.device)
+                             for _ in range(slots)]
+                torch.cuda.synchronize(self.device)
+                obj = [[reduce_tensor(b) for b in self.bufs]]
+        except Exception as e:  # agreed below
+            err = e
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+            if rank != 0 and obj[0] is not None:
+                try:
+                    with torch.cuda.device(self.device):
+                        self.bufs = [fn(*args) for fn, args in obj[0]]
+                except Exception as e:
+                    err, self.bufs = e, None
+        nccl = world > 1 and dist.get_backend() == "nccl"
+        self._flag = torch.ones(1, dtype=torch.int32, device=self.device if nccl else "cpu")
+        ok = torch.tensor([0 if (err is not None or self.bufs is None) else 1], dtype=torch.int32,
+                          device=self._flag.device)
+        if world > 1:
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            self.bufs = None
+            raise RuntimeError(f"peer-memory gather unavailable: {err!r}")
+
+    def mine(self, slot: int) -> torch.Tensor:
+        """This rank's slice of slot `slot` (memory of rank 0's device)."""
+        b = self.bufs[slot]
+        return b[self.rank * self.stride:self.rank * self.stride + self.nbytes]
+
+    def gathered(self, slot: int):
+        """Rank 0: the list of per-rank payloads of slot `slot` (views, no copy)."""
+        if self.rank != 0:
+            return None
+        b = self.bufs[slot]
+        return [b[r * self.stride:r * self.stride + self.nbytes] for r in range(self.world)]
+
+    def fence(self):
+        """Orders 'every rank's step has completed' after the work already enqueued on the
+        current stream (NCCL) or after a device synchronize (gloo, CPU tests)."""
+        if self.world <= 1:
+            return
+        if dist.get_backend() != "nccl":
+            torch.cuda.synchronize(self.device)
+        dist.all_reduce(self._flag, op=dist.ReduceOp.MAX)
+
+    def close(self):
+        self.bufs = None
