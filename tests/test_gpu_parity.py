@@ -101,6 +101,37 @@ def test_census_cost_aggregate_wta_lr(orc, dev, shape):
     g.close()
 
 
+# Widths around the row loop's unrolled block (CPL positions), its tail, and the backward
+# sweep's WTA record period (32 positions; 30 for 6 cells per lane): W below one block, exact
+# multiples, one more / one less, for every cells-per-lane variant; a few rows only (the
+# oracle's cost grows with W H D).  The production path (fused sweeps, sub-pixel + store block
+# at the block ends) is compared with the oracle's LR-checked maps.
+WIDTHS = [
+    (16, 2, (1, 2, 3, 31, 32, 33, 64, 65)),
+    (128, 4, (1, 3, 4, 5, 31, 32, 33, 35, 36, 64, 67)),
+    (192, 6, (1, 5, 6, 7, 29, 30, 31, 36, 59, 60, 61, 66, 90)),
+    (256, 8, (1, 7, 8, 9, 31, 32, 33, 40, 63, 64, 65)),
+]
+
+
+@pytest.mark.parametrize("D,cpl,widths", WIDTHS, ids=lambda v: str(v) if isinstance(v, int) else "w")
+def test_disparity_widths_around_block_and_period(orc, dev, D, cpl, widths):
+    H = 5
+    for W in widths:
+        L, R = synth.random_pair(W, H, seed=1000 * cpl + W)
+        g = make_sgm(W, H, D, 9, 7, 7, 86)
+        assert g.geometry()["cells_per_lane"] == cpl
+        fi, fsub, fv = g.disparity(g.upload_image(L), g.upload_image(R))
+        ocl, ocr = orc.census(L, 9, 7), orc.census(R, 9, 7)
+        dl, dls = orc.sgm_view(ocl, ocr, D, -1, 62, 7, 86)[:2]
+        dr = orc.sgm_view(ocr, ocl, D, +1, 62, 7, 86)[0]
+        oi, osub, ov = orc.lr_check(dl, dls, dr, 1)
+        assert np.array_equal(_np(fv), ov), (D, W)
+        assert np.array_equal(_np(fi), oi), (D, W)
+        assert np.abs(_np(fsub) - osub).max() <= SUB_TOL, (D, W)
+        g.close()
+
+
 def test_aggregate_invariants_on_gpu(orc, dev):
     """P1 = P2 = 0 => S = 8C (north-star invariant) on the GPU path too."""
     W, H, D = 120, 40, 64
