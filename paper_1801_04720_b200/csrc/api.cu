@@ -617,7 +617,11 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, bool stream, const u
     int16_t *di = out->disp_int ? out->disp_int : h->lr_int;
     float *ds = out->disp_sub ? out->disp_sub : h->lr_sub;
     uint8_t *dv = out->disp_valid ? out->disp_valid : h->lr_valid;
-    {
+    // No disparity map asked for: the LR check is fused into the combination kernel (the
+    // LR-checked maps are never materialised, one launch less).  SGM_DEBUG_FLAGS & 64 keeps
+    // the separate LR kernel (A/B, parity of the two forms).
+    const bool fuse_lr = !out->disp_int && !out->disp_sub && !out->disp_valid && !(h->debug_flags & 64);
+    if (!fuse_lr) {
         sgm::LrParams p{};
         p.W = W; p.H = H; p.T = h->prm.lr_threshold; p.invalid = h->prm.invalid_disp;
         p.npairs = npairs;
@@ -641,6 +645,11 @@ static sgm_status scene_flow_impl(sgm_handle *h, int32_t n, bool stream, const u
         }
         p.sf = out->sf; p.valid_sf = out->valid_sf;
         p.p0 = out->p0; p.dp = want3d ? out->dp : nullptr; p.valid_3d = out->valid_3d;
+        if (fuse_lr) {
+            p.raw_int = h->dint; p.raw_sub = h->dsub; p.view_stride = npx;
+            p.pair_step = stream ? 1 : 2; p.T = h->prm.lr_threshold;
+            p.invalid = float(h->prm.invalid_disp);
+        }
         e = sgm::launch_combine(p, st);
         if (e != cudaSuccess) return from_cuda(e);
         ++h->launches;

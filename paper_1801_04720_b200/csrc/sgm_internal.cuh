@@ -122,6 +122,13 @@ struct CombineParams {
     const float *flow; const uint8_t *flow_valid;
     float f, B, cx, cy, fB;
     float *sf, *p0, *dp; uint8_t *valid_sf, *valid_3d;
+    // fused LR check (raw_int != nullptr): the LR-checked maps are not materialised; the
+    // kernel applies the check (G13) to the raw WTA maps of the views [2 * pair + side] at the
+    // pixels it reads.  Quad q uses pairs q * pair_step (t) and q * pair_step + 1 (t+1).
+    const int16_t *raw_int; const float *raw_sub;
+    long long view_stride;                 // elements between consecutive views
+    int pair_step, T;
+    float invalid;
 };
 
 struct EvalParams {

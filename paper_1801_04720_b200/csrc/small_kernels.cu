@@ -82,6 +82,13 @@ __global__ void lr_kernel(const LrParams p) {
 // ------------------------------------------------------------------ combination + 3D
 // One thread per pixel, float4 stores.  Validity decisions are taken in float32 exactly
 // like the oracle's (x' = (float)x + u, floor, fractional part, taps with nonzero weight).
+//
+// LRF (production path when the caller takes no disparity maps): the LR check (G13) is
+// fused in -- validity and value of D0 at x and of D1 at the four taps are derived from the raw
+// WTA maps on the fly (valid iff x - d_L >= 0 and |d_L - d_R(x - d_L)| <= T; an invalid tap's
+// value is invalid_disp, exactly what lr_kernel would have stored), so the LR-checked maps are
+// never written or read and the LR launch disappears.  Same arithmetic, same results.
+template <bool LRF>
 __global__ void combine_kernel(const CombineParams p) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= p.W) return;
@@ -91,11 +98,21 @@ __global__ void combine_kernel(const CombineParams p) {
     const long long px = (long long)y * p.W + x, idx = q * npx + px;
     {
         const float2 uv = reinterpret_cast<const float2 *>(p.flow)[idx];
-        const float *d0 = p.d0 + q * p.disp_stride;
-        const float *d1 = p.d1 + q * p.disp_stride;
-        const uint8_t *v0 = p.v0 + q * p.disp_stride;
-        const uint8_t *v1 = p.v1 + q * p.disp_stride;
-        bool ok = (p.flow_valid == nullptr || p.flow_valid[idx]) && v0[px];
+        const float *d0 = LRF ? nullptr : p.d0 + q * p.disp_stride;
+        const float *d1 = LRF ? nullptr : p.d1 + q * p.disp_stride;
+        const uint8_t *v0 = LRF ? nullptr : p.v0 + q * p.disp_stride;
+        const uint8_t *v1 = LRF ? nullptr : p.v1 + q * p.disp_stride;
+        // fused LR: raw maps of the left / right views of the two pairs of this quad
+        const long long vw0 = LRF ? 2 * (q * p.pair_step) * p.view_stride : 0;
+        const int16_t *l0 = LRF ? p.raw_int + vw0 : nullptr, *l1 = LRF ? l0 + 2 * p.view_stride : nullptr;
+        const float *s0 = LRF ? p.raw_sub + vw0 : nullptr, *s1 = LRF ? s0 + 2 * p.view_stride : nullptr;
+        auto lr_ok = [&](const int16_t *L, long long row, int xx) {
+            const int d = L[row + xx];
+            const int xr = xx - d;
+            return xr >= 0 && xr < p.W && abs(d - int(L[p.view_stride + row + xr])) <= p.T;
+        };
+        bool ok = (p.flow_valid == nullptr || p.flow_valid[idx]) &&
+                  (LRF ? lr_ok(l0, px - x, x) : bool(v0[px]));
         const float xp = __fadd_rn(float(x), uv.x), yp = __fadd_rn(float(y), uv.y);
         ok = ok && (xp >= 0.f && xp <= float(p.W - 1) && yp >= 0.f && yp <= float(p.H - 1));
         float d1w = 0.f, d0v = 0.f;
@@ -105,24 +122,35 @@ __global__ void combine_kernel(const CombineParams p) {
             const int x1 = min(x0 + 1, p.W - 1), y1 = min(y0 + 1, p.H - 1);
             const long long q00 = (long long)y0 * p.W + x0, q10 = (long long)y0 * p.W + x1;
             const long long q01 = (long long)y1 * p.W + x0, q11 = (long long)y1 * p.W + x1;
+            bool t00, t10, t01, t11;
+            if (LRF) {
+                const long long r0 = (long long)y0 * p.W, r1 = (long long)y1 * p.W;
+                t00 = lr_ok(l1, r0, x0); t10 = lr_ok(l1, r0, x1);
+                t01 = lr_ok(l1, r1, x0); t11 = lr_ok(l1, r1, x1);
+            } else {
+                t00 = v1[q00]; t10 = v1[q10]; t01 = v1[q01]; t11 = v1[q11];
+            }
             bool tv;
             if (p.rule == 1) {
-                tv = v1[q00] && v1[q10] && v1[q01] && v1[q11];
+                tv = t00 && t10 && t01 && t11;
             } else {
-                tv = v1[q00] && (fx == 0.f || v1[q10]) && (fy == 0.f || v1[q01]) &&
-                     (fx == 0.f || fy == 0.f || v1[q11]);
+                tv = t00 && (fx == 0.f || t10) && (fy == 0.f || t01) && (fx == 0.f || fy == 0.f || t11);
             }
             ok = tv;
             if (ok) {
                 // Eq. (5) in the paper's term order; zero-weight taps contribute exactly 0
                 // (their values are finite: invalid disparities are -1, never NaN, G14).
                 const float ax = fx, ay = fy, bx = 1.f - fx, by = 1.f - fy;
-                float acc = __fmul_rn(__fmul_rn(d1[q00], bx), by);
-                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(d1[q10], ax), by));
-                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(d1[q01], bx), ay));
-                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(d1[q11], ax), ay));
+                const float e00 = LRF ? s1[q00] : d1[q00];
+                const float e10 = LRF ? (t10 ? s1[q10] : p.invalid) : d1[q10];
+                const float e01 = LRF ? (t01 ? s1[q01] : p.invalid) : d1[q01];
+                const float e11 = LRF ? (t11 ? s1[q11] : p.invalid) : d1[q11];
+                float acc = __fmul_rn(__fmul_rn(e00, bx), by);
+                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(e10, ax), by));
+                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(e01, bx), ay));
+                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(e11, ax), ay));
                 d1w = acc;
-                d0v = d0[px];
+                d0v = LRF ? s0[px] : d0[px];
             }
         }
         float4 s = ok ? make_float4(uv.x, uv.y, d0v, d1w) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -197,7 +225,9 @@ cudaError_t launch_lr(const LrParams &p, cudaStream_t st) {
 
 cudaError_t launch_combine(const CombineParams &p, cudaStream_t st) {
     if (p.nquads < 1 || p.nquads > 65535 || p.H > 65535) return cudaErrorInvalidValue;
-    combine_kernel<<<dim3((p.W + 127) / 128, p.H, p.nquads), 128, 0, st>>>(p);
+    const dim3 grid((p.W + 127) / 128, p.H, p.nquads);
+    if (p.raw_int != nullptr) combine_kernel<true><<<grid, 128, 0, st>>>(p);
+    else combine_kernel<false><<<grid, 128, 0, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -438,3 +438,38 @@ def test_random_small_instances(orc, dev):
             torch.cuda.synchronize()
             assert np.array_equal(_np(gS).astype(np.uint32), S), (it, view, W, H, D)
         g.close()
+
+
+@pytest.mark.parametrize("name,n,rule", [("tiny", 3, 0), ("tiny", 2, 1), ("driving", 2, 0), ("wide", 1, 0)])
+def test_fused_lr_combination_equals_separate_kernels(dev, name, n, rule):
+    """Without disparity outputs sgm_scene_flow fuses the LR check into the combination
+    kernel (4 launches, the LR-checked maps never materialised); the results must equal, bit
+    for bit, those of the 5-launch form (which the other tests compare with the oracle) --
+    quad and streaming mode, both bilinear rules, with a flow mask."""
+    from paper_1801_04720_b200 import SGM, Camera, stack_quads, stack_video
+    cfg = synth.CONFIGS[name]
+    prm = synth.sgm_params(cfg)
+    g = SGM(cfg.W, cfg.H, cfg.D, cfg.cw, cfg.ch, cfg.P1, cfg.P2, cfg.T, -1, rule, n, 0)
+    cam = Camera(prm["f"], prm["B"], prm["cx"], prm["cy"])
+    quads = [synth.make_quad(cfg, 40 + k) for k in range(n)]
+    imgs, flow = stack_quads(quads, g.pitch, dev)
+    rng = np.random.default_rng(5)
+    fmask = torch.from_numpy((rng.uniform(size=(n, cfg.H, cfg.W)) < 0.9).astype(np.uint8)).to(dev)
+    keys = ("sf", "valid_sf", "p0", "dp", "valid_3d")
+    for mask in (None, fmask):
+        ref = g.scene_flow(imgs, flow, cam, flow_valid=mask)              # with disparity maps
+        n0 = g.launch_count()
+        out = g.scene_flow(imgs, flow, cam, g.alloc_outputs(n, with_disp=False), flow_valid=mask)
+        torch.cuda.synchronize()
+        assert g.launch_count() - n0 == 4
+        for k in keys:
+            assert torch.equal(out[k], ref[k]), (k, mask is not None)
+    if name == "tiny":
+        video = synth.make_video(cfg, n, 7)
+        vi, vf = stack_video(video, g.pitch, dev)
+        ref = g.scene_flow_stream(vi, vf, cam)
+        out = g.scene_flow_stream(vi, vf, cam, g.alloc_outputs(n, with_disp=False, stream_mode=True))
+        torch.cuda.synchronize()
+        for k in keys:
+            assert torch.equal(out[k], ref[k]), ("stream", k)
+    g.close()

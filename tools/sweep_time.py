@@ -28,7 +28,7 @@ def main():
     g = SGM.from_config(cfg, max_batch=n)
     imgs, flow = stack_quads(quads, g.pitch, dev)
     cam = Camera(prm["f"], prm["B"], prm["cx"], prm["cy"])
-    out = g.alloc_outputs(n)
+    out = g.alloc_outputs(n, with_disp=not os.environ.get("SWEEP_NO_DISP"))
     st = torch.cuda.Stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     with torch.cuda.stream(st):
