@@ -790,7 +790,12 @@ cudaError_t ff_launch_lift(const FFFields &F, const int32_t *coarse, int Wc, int
     return cudaGetLastError();
 }
 
-constexpr int kPropNW = 16;
+// rows (warps) per propagation CTA; measured on the 8 bench pairs (propagation ms): 12 rows
+// 52.2, 16 rows 40.9, 20 rows 46.1 (96 registers), 24 rows 50.3 (80 registers)
+#ifndef FF_PROP_NW
+#define FF_PROP_NW 16
+#endif
+constexpr int kPropNW = FF_PROP_NW;
 
 size_t ff_prop_smem(int W) {
     (void)W;
