@@ -733,7 +733,11 @@ static sgm_status scene_flow_host_impl(sgm_handle *h, int32_t n, bool stream_mod
     dev.sf = sg.sf;
     dev.valid_sf = sg.vsf;
     if (want3d) { dev.p0 = out->p0 ? sg.p0 : nullptr; dev.dp = sg.dp; dev.valid_3d = sg.v3; }
-    dev.disp_int = sg.di; dev.disp_sub = sg.ds; dev.disp_valid = sg.dv;
+    // (no disparity map requested: none is staged, and the LR check runs fused in the
+    // combination kernel)
+    if (out->disp_int || out->disp_sub || out->disp_valid) {
+        dev.disp_int = sg.di; dev.disp_sub = sg.ds; dev.disp_valid = sg.dv;
+    }
     sgm_status s = scene_flow_impl(h, n, stream_mode, sg.img, h->stage_pitch, sg.flow,
                                    flow_valid ? sg.fvalid : nullptr, cam, &dev, h->s_comp,
                                    h->sync_host);

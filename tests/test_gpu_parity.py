@@ -381,6 +381,15 @@ def test_host_entry_point_matches_device(dev):
         for j, i in enumerate(sel):
             for k in ho:
                 assert torch.equal(ho[k][j], ref[k][i].cpu()), (sel, k)
+    # without disparity outputs the host entry stages none and runs the fused LR + combination
+    # form (4 kernels + the re-pitch): same bytes
+    hno = g.alloc_outputs(n, pinned_host=True, with_disp=False)
+    n0 = g.launch_count()
+    g.scene_flow_host(himg, hflow, cam, hno)
+    torch.cuda.synchronize()
+    assert g.launch_count() - n0 == 5
+    for k in hno:
+        assert torch.equal(hno[k], ref[k].cpu()), k
     g.close()
 
 
